@@ -1,0 +1,120 @@
+/*
+ * prefill_sm100.h — C-ABI of libprefill_sm100.so, the B200 (sm_100a) hot path of prefill-only
+ * shared-prefix relevance scoring (arxiv 2510.22101, reference package `prefrank`).
+ *
+ * The reference ships no code for this path: its interface is specified in
+ * /root/reference/SPEC.md (model :172-238, prefixcache :240-309, scoring :311-343).  Each entry
+ * point below cites the reference operation it replaces.  All pointers are DEVICE pointers unless
+ * a function name ends in `_host`; all buffers are caller-owned (the library never cudaMallocs).
+ * Return value: 0 on success, negative on error; the message is in pf_last_error().
+ *
+ * Error codes:  -1 bad handle/argument, -2 unsupported shape, -3 TMA descriptor encode failed,
+ *               -4 CUDA launch/runtime error, -5 workspace too small, -6 non-finite logits
+ *               ("non-finite logits" error of relevance_score).
+ */
+#ifndef PREFILL_SM100_H
+#define PREFILL_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PF_API __attribute__((visibility("default")))
+#else
+#define PF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* pf_stream_t; /* == cudaStream_t */
+typedef struct pf_model pf_model;        /* opaque: config + cached weight TMA descriptors */
+
+/*
+ * Model description — SPEC.md:177-184 ModelConfig/Weights, with the explicit d_head and padded
+ * FFN width the B200 layout needs.  Weights are device tensors in the
+ * K-major ("[out x in]") layout the tcgen05 GEMMs read:
+ *   embedding  bf16 [vocab_size x d_model]
+ *   w_qkv[l]   bf16 [(n_heads + 2 n_kv_heads) d_head x d_model]   rows: q heads | k heads | v heads
+ *   w_o[l]     bf16 [d_model x n_heads d_head]
+ *   w_gu[l]    bf16 [2 d_ff_pad x d_model]   per 128-neuron block j: 128 gate rows then 128 up rows
+ *   w_down[l]  bf16 [d_model x d_ff_pad]     columns >= d_ff are zero (pruned/padded neurons)
+ *   ln_attn[l], ln_mlp[l], ln_final : fp32 [d_model] RMSNorm scales
+ *   w_yes, w_no: fp32 [d_model] — columns yes_id / no_id of the [d_model x vocab] output head
+ *   rope_cos, rope_sin: fp32 [max_seq x d_head/2]  (theta^(-2i/d_head) * pos, rotate-half)
+ */
+typedef struct pf_model_desc {
+  int n_layers, d_model, n_heads, n_kv_heads, d_head, d_ff, d_ff_pad, vocab_size, max_seq;
+  float rms_eps;
+  const void* embedding;
+  const void* const* w_qkv;
+  const void* const* w_o;
+  const void* const* w_gu;
+  const void* const* w_down;
+  const float* const* ln_attn;
+  const float* const* ln_mlp;
+  const float* ln_final;
+  const float* w_yes;
+  const float* w_no;
+  const float* rope_cos;
+  const float* rope_sin;
+} pf_model_desc;
+
+/* Packed request batch (SPEC.md:245-263 SharedBatch, laid out flat):
+ *   ids[T], pos[T]           token ids and absolute RoPE positions (prefix 0..P-1, each suffix P..)
+ *   segs[n_seg][4]           {kv_off, kv_len, q_off, q_len}: query rows [q_off, q_off+q_len) attend
+ *                            densely to rows [kv_off, kv_off+kv_len) (the shared prefix) and
+ *                            causally to themselves.  A request's prefix is {q_off, 0, q_off, P}.
+ *   work[n_work][4]          {seg, q_tile, 0, 0}: one entry per 128-row query tile of a segment
+ *   last_idx[n_items]        packed row of each item's last token
+ */
+
+/* Lifecycle.  Replaces: init_weights/Weights as the device-resident form. */
+PF_API int pf_model_create(const pf_model_desc* desc, pf_model** out);
+PF_API int pf_model_destroy(pf_model* model);
+
+/* Bytes of device workspace pf_score needs for T packed tokens and n_items items. */
+PF_API size_t pf_workspace_bytes(const pf_model* model, int T, int n_items);
+
+/* The whole packed forward: embed -> L x [RMSNorm, QKV+RoPE, shared-prefix attention,
+ * O+residual, RMSNorm, gate/up+SwiGLU, down+residual] -> last-token RMSNorm -> yes/no head ->
+ * sigmoid.  Replaces score_shared_batch + relevance_score;
+ * logits2[n_items][2] = (logit_yes, logit_no), p_yes[n_items].  Device pointers throughout;
+ * asynchronous on `stream`.  bad_flag (device int) is OR-ed with 1 on non-finite logits. */
+PF_API int pf_score(pf_model* model, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+             int n_seg, const int32_t* work, int n_work, const int32_t* last_idx, int n_items,
+             int T, void* workspace, size_t ws_bytes, float* logits2, float* p_yes,
+             int* bad_flag, pf_stream_t stream);
+
+/* Same, with HOST input/output buffers: H2D copies of the packed batch and D2H copy of the
+ * scores are inside the call, which returns after the stream synchronises (-6 on non-finite). */
+PF_API int pf_score_host(pf_model* model, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+                  int n_seg, const int32_t* work, int n_work, const int32_t* last_idx,
+                  int n_items, int T, void* workspace, size_t ws_bytes, float* logits2_host,
+                  float* p_yes_host, pf_stream_t stream);
+
+/* Per-op entry points (unit parity tests). */
+/* C = A[MxK] . B[NxK]^T with epilogue 0 bf16, 1 bf16+RoPE, 2 SwiGLU(bf16, N/2 cols),
+ * 3 fp32 C += (residual add). */
+PF_API int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
+                 int K, int epilogue, const int32_t* pos, const float* rope_cos,
+                 const float* rope_sin, int rope_heads, pf_stream_t stream);
+PF_API int pf_embed(const int32_t* ids, const void* emb, float* resid, int T, int d, pf_stream_t stream);
+PF_API int pf_rmsnorm(const float* x, const float* gamma, void* y_bf16, int T, int d, float eps,
+               pf_stream_t stream);
+PF_API int pf_prefix_attention(const void* qkv, void* out, int T, int n_heads, int n_kv_heads,
+                        int d_head, const int32_t* segs, const int32_t* work, int n_work,
+                        pf_stream_t stream);
+PF_API int pf_head_last_token(const float* resid, const int32_t* last_idx, int n_items, int d,
+                       const float* final_gamma, const float* w_yes, const float* w_no,
+                       float eps, float* logits2, float* p_yes, int* bad_flag,
+                       pf_stream_t stream);
+
+PF_API const char* pf_last_error(void);
+PF_API const char* pf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PREFILL_SM100_H */

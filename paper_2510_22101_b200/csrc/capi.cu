@@ -1,0 +1,311 @@
+// C-ABI of libprefill_sm100.so (include/prefill_sm100.h): model handle, workspace layout,
+// the packed forward (pf_score), the host-buffer variant and per-op entry points.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+#include <cudaTypedefs.h>
+#include "pf_internal.h"
+#include "../../include/prefill_sm100.h"
+
+namespace pf {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_tmap_2d(CUtensorMap* out, const void* base, int elem_bytes, uint64_t rows, uint64_t cols,
+                  uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128) {
+  auto enc = get_encode();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return false; }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * elem_bytes) % 16 != 0) {
+    set_error("tensor map: base %p / row stride %llu B not 16-byte aligned", base,
+              (unsigned long long)(ld * elem_bytes));
+    return false;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * (uint64_t)elem_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapDataType dt = elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUresult r = enc(out, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%llu cols=%llu ld=%llu box=%ux%u", (int)r,
+              (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)ld, box_rows,
+              box_cols);
+    return false;
+  }
+  return true;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+struct pf_model {
+  pf_model_desc d;
+  std::vector<const void*> w_qkv, w_o, w_gu, w_down;
+  std::vector<const float*> ln_attn, ln_mlp;
+  std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;  // cached weight (B operand) maps
+  int qkv_n, attn_k;
+};
+
+namespace {
+
+constexpr size_t kAlign = 1024;
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct Workspace {
+  float* resid;
+  void* xn;
+  void* qkv;
+  void* attn;
+  void* hbuf;
+  // device copies of host inputs/outputs (pf_score_host)
+  int32_t *ids, *pos, *segs, *work, *last_idx;
+  float *logits2, *p_yes;
+  int* bad;
+  size_t total;
+};
+
+Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, uint8_t* base) {
+  const pf_model_desc& d = m->d;
+  Workspace w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { uint8_t* p = base + off; off = align_up(off + bytes); return p; };
+  w.resid = reinterpret_cast<float*>(take((size_t)T * d.d_model * 4));
+  w.xn = take((size_t)T * d.d_model * 2);
+  w.qkv = take((size_t)T * m->qkv_n * 2);
+  w.attn = take((size_t)T * m->attn_k * 2);
+  w.hbuf = take((size_t)T * d.d_ff_pad * 2);
+  w.ids = reinterpret_cast<int32_t*>(take((size_t)T * 4));
+  w.pos = reinterpret_cast<int32_t*>(take((size_t)T * 4));
+  w.segs = reinterpret_cast<int32_t*>(take((size_t)n_seg * 16));
+  w.work = reinterpret_cast<int32_t*>(take((size_t)n_work * 16));
+  w.last_idx = reinterpret_cast<int32_t*>(take((size_t)n_items * 4));
+  w.logits2 = reinterpret_cast<float*>(take((size_t)n_items * 8));
+  w.p_yes = reinterpret_cast<float*>(take((size_t)n_items * 4));
+  w.bad = reinterpret_cast<int*>(take(16));
+  w.total = off;
+  return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pf_last_error(void) { return g_err; }
+const char* pf_version(void) { return "prefill_sm100 0.1 (tcgen05 bf16, sm_100a)"; }
+
+int pf_model_create(const pf_model_desc* desc, pf_model** out) {
+  if (!desc || !out) return fail(-1, "pf_model_create: null argument");
+  const pf_model_desc& d = *desc;
+  if (d.n_layers < 1 || d.d_model % 128 != 0 || d.n_heads < 1 || d.n_kv_heads < 1 ||
+      d.n_heads % d.n_kv_heads != 0)
+    return fail(-2, "pf_model_create: invalid dims (L=%d d=%d H=%d Hkv=%d)", d.n_layers, d.d_model,
+                d.n_heads, d.n_kv_heads);
+  if (d.d_head != 128) return fail(-2, "pf_model_create: d_head must be 128 (got %d)", d.d_head);
+  if (d.d_ff_pad % 128 != 0 || d.d_ff_pad < d.d_ff)
+    return fail(-2, "pf_model_create: d_ff_pad=%d must be a multiple of 128 >= d_ff=%d", d.d_ff_pad, d.d_ff);
+  pf_model* m = new (std::nothrow) pf_model();
+  if (!m) return fail(-1, "pf_model_create: out of host memory");
+  m->d = d;
+  m->qkv_n = (d.n_heads + 2 * d.n_kv_heads) * d.d_head;
+  m->attn_k = d.n_heads * d.d_head;
+  const int L = d.n_layers;
+  m->w_qkv.assign(d.w_qkv, d.w_qkv + L);
+  m->w_o.assign(d.w_o, d.w_o + L);
+  m->w_gu.assign(d.w_gu, d.w_gu + L);
+  m->w_down.assign(d.w_down, d.w_down + L);
+  m->ln_attn.assign(d.ln_attn, d.ln_attn + L);
+  m->ln_mlp.assign(d.ln_mlp, d.ln_mlp + L);
+  m->d.w_qkv = m->w_qkv.data();
+  m->d.w_o = m->w_o.data();
+  m->d.w_gu = m->w_gu.data();
+  m->d.w_down = m->w_down.data();
+  m->d.ln_attn = m->ln_attn.data();
+  m->d.ln_mlp = m->ln_mlp.data();
+  m->tm_qkv.resize(L);
+  m->tm_o.resize(L);
+  m->tm_gu.resize(L);
+  m->tm_down.resize(L);
+  for (int l = 0; l < L; ++l) {
+    bool ok = make_tmap_2d(&m->tm_qkv[l], m->w_qkv[l], 2, m->qkv_n, d.d_model, d.d_model, 256, 64, true) &&
+              make_tmap_2d(&m->tm_o[l], m->w_o[l], 2, d.d_model, m->attn_k, m->attn_k, 256, 64, true) &&
+              make_tmap_2d(&m->tm_gu[l], m->w_gu[l], 2, 2 * d.d_ff_pad, d.d_model, d.d_model, 256, 64, true) &&
+              make_tmap_2d(&m->tm_down[l], m->w_down[l], 2, d.d_model, d.d_ff_pad, d.d_ff_pad, 256, 64, true);
+    if (!ok) { delete m; return -3; }
+  }
+  *out = m;
+  return 0;
+}
+
+int pf_model_destroy(pf_model* model) {
+  delete model;
+  return 0;
+}
+
+size_t pf_workspace_bytes(const pf_model* model, int T, int n_items) {
+  if (!model) return 0;
+  // segs/work are bounded by T (every segment and tile holds >= 1 token)
+  return layout(model, T, n_items, T, T, nullptr).total + kAlign;
+}
+
+static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+                       int n_seg, const int32_t* work, int n_work, const int32_t* last_idx,
+                       int n_items, int T, const Workspace& w, float* logits2, float* p_yes,
+                       int* bad, cudaStream_t st) {
+  (void)n_seg;
+  const pf_model_desc& d = m->d;
+  const float eps = d.rms_eps;
+  int rc = launch_embed(ids, d.embedding, w.resid, T, d.d_model, d.vocab_size, st);
+  if (rc) return rc;
+  for (int l = 0; l < d.n_layers; ++l) {
+    if ((rc = launch_rmsnorm(w.resid, d.ln_attn[l], w.xn, T, d.d_model, eps, st))) return rc;
+    GemmDesc g{};
+    g.A = w.xn; g.lda = d.d_model; g.B = d.w_qkv[l]; g.ldb = d.d_model;
+    g.C = w.qkv; g.ldc = m->qkv_n; g.M = T; g.N = m->qkv_n; g.K = d.d_model;
+    g.epilogue = EPI_ROPE_BF16; g.pos = pos; g.rope_cos = d.rope_cos; g.rope_sin = d.rope_sin;
+    g.rope_heads = d.n_heads + d.n_kv_heads; g.max_seq = d.max_seq;
+    if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
+    AttnDesc a{};
+    a.qkv = w.qkv; a.out = w.attn; a.T = T; a.H = d.n_heads; a.Hkv = d.n_kv_heads; a.dh = d.d_head;
+    a.work = work; a.n_work = n_work; a.segs = segs; a.scale = 1.0f / sqrtf((float)d.d_head);
+    if ((rc = launch_attention(a, st))) return rc;
+    GemmDesc o{};
+    o.A = w.attn; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
+    o.C = w.resid; o.ldc = d.d_model; o.M = T; o.N = d.d_model; o.K = m->attn_k;
+    o.epilogue = EPI_RESID_ADD;
+    if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
+    if ((rc = launch_rmsnorm(w.resid, d.ln_mlp[l], w.xn, T, d.d_model, eps, st))) return rc;
+    GemmDesc gu{};
+    gu.A = w.xn; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
+    gu.C = w.hbuf; gu.ldc = d.d_ff_pad; gu.M = T; gu.N = 2 * d.d_ff_pad; gu.K = d.d_model;
+    gu.epilogue = EPI_SWIGLU;
+    if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
+    GemmDesc dn{};
+    dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
+    dn.C = w.resid; dn.ldc = d.d_model; dn.M = T; dn.N = d.d_model; dn.K = d.d_ff_pad;
+    dn.epilogue = EPI_RESID_ADD;
+    if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
+  }
+  return launch_head(w.resid, last_idx, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
+                     logits2, p_yes, bad, st);
+}
+
+static int check_args(pf_model* m, int T, int n_items, int n_seg, int n_work, void* ws, size_t ws_bytes,
+                      size_t* need) {
+  if (!m) return fail(-1, "null model handle");
+  if (T < 1 || n_items < 1 || n_seg < 1 || n_work < 1 || n_seg > T || n_work > T)
+    return fail(-1, "bad batch sizes T=%d items=%d segs=%d work=%d", T, n_items, n_seg, n_work);
+  *need = layout(m, T, n_items, T, T, nullptr).total;
+  if (!ws || ws_bytes < *need)
+    return fail(-5, "workspace too small: %zu < %zu bytes", ws_bytes, *need);
+  if ((reinterpret_cast<uintptr_t>(ws) & (kAlign - 1)) != 0)
+    return fail(-1, "workspace must be %zu-byte aligned", kAlign);
+  return 0;
+}
+
+int pf_score(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs, int n_seg,
+             const int32_t* work, int n_work, const int32_t* last_idx, int n_items, int T,
+             void* workspace, size_t ws_bytes, float* logits2, float* p_yes, int* bad_flag,
+             pf_stream_t stream) {
+  size_t need = 0;
+  int rc = check_args(m, T, n_items, n_seg, n_work, workspace, ws_bytes, &need);
+  if (rc) return rc;
+  Workspace w = layout(m, T, n_items, T, T, static_cast<uint8_t*>(workspace));
+  return run_forward(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, w, logits2,
+                     p_yes, bad_flag, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_score_host(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+                  int n_seg, const int32_t* work, int n_work, const int32_t* last_idx, int n_items,
+                  int T, void* workspace, size_t ws_bytes, float* logits2_host, float* p_yes_host,
+                  pf_stream_t stream) {
+  size_t need = 0;
+  int rc = check_args(m, T, n_items, n_seg, n_work, workspace, ws_bytes, &need);
+  if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace w = layout(m, T, n_items, T, T, static_cast<uint8_t*>(workspace));
+  cudaMemcpyAsync(w.ids, ids, (size_t)T * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(w.pos, pos, (size_t)T * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(w.segs, segs, (size_t)n_seg * 16, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(w.work, work, (size_t)n_work * 16, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(w.last_idx, last_idx, (size_t)n_items * 4, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(w.bad, 0, 4, st);
+  rc = run_forward(m, w.ids, w.pos, w.segs, n_seg, w.work, n_work, w.last_idx, n_items, T, w,
+                   w.logits2, w.p_yes, w.bad, st);
+  if (rc) return rc;
+  int bad = 0;
+  cudaMemcpyAsync(logits2_host, w.logits2, (size_t)n_items * 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(p_yes_host, w.p_yes, (size_t)n_items * 4, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&bad, w.bad, 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(-4, "pf_score_host: %s", cudaGetErrorString(e));
+  if (bad) return fail(-6, "non-finite logits");
+  return 0;
+}
+
+int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
+                 int K, int epilogue, const int32_t* pos, const float* rope_cos,
+                 const float* rope_sin, int rope_heads, pf_stream_t stream) {
+  GemmDesc g{};
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc; g.M = M; g.N = N; g.K = K;
+  g.epilogue = epilogue; g.pos = pos; g.rope_cos = rope_cos; g.rope_sin = rope_sin;
+  g.rope_heads = rope_heads;
+  return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_embed(const int32_t* ids, const void* emb, float* resid, int T, int d, pf_stream_t stream) {
+  return launch_embed(ids, emb, resid, T, d, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_rmsnorm(const float* x, const float* gamma, void* y, int T, int d, float eps, pf_stream_t stream) {
+  return launch_rmsnorm(x, gamma, y, T, d, eps, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_prefix_attention(const void* qkv, void* out, int T, int n_heads, int n_kv_heads, int d_head,
+                        const int32_t* segs, const int32_t* work, int n_work, pf_stream_t stream) {
+  AttnDesc a{};
+  a.qkv = qkv; a.out = out; a.T = T; a.H = n_heads; a.Hkv = n_kv_heads; a.dh = d_head;
+  a.segs = segs; a.work = work; a.n_work = n_work; a.scale = 1.0f / sqrtf((float)d_head);
+  return launch_attention(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_head_last_token(const float* resid, const int32_t* last_idx, int n_items, int d,
+                       const float* g, const float* w_yes, const float* w_no, float eps,
+                       float* logits2, float* p_yes, int* bad, pf_stream_t stream) {
+  return launch_head(resid, last_idx, n_items, d, g, w_yes, w_no, eps, logits2, p_yes, bad,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// HBM-bound kernels of the packed prefill:
+//   embed_kernel    x[t] = float(E[id[t]])                  (bf16 table -> fp32 residual stream)
+//   rmsnorm_kernel  y = bf16(x * rsqrt(mean(x^2) + eps) * g) (fp32 residual -> bf16 GEMM operand)
+//   head_kernel     last-token gather -> final RMSNorm -> 2-row yes/no head -> sigmoid
+// One warp per row, 16-byte vector loads/stores, row kept in registers (single HBM read).
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "ptx.cuh"
+#include "pf_internal.h"
+
+namespace pf {
+
+PF_DEVICE float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- embedding gather
+// VPL = bf16 uint4 (8 values) per lane: d = VPL * 256.
+__global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ ids,
+                                                    const __nv_bfloat16* __restrict__ emb,
+                                                    float* __restrict__ resid, int T, int d) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int id = __ldg(ids + t);
+  const uint4* src = reinterpret_cast<const uint4*>(emb + (size_t)id * d);
+  float4* dst = reinterpret_cast<float4*>(resid + (size_t)t * d);
+  for (int i = lane; i < d / 8; i += 32) {
+    const uint4 u = __ldg(src + i);
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const float2 a = __bfloat1622float2(p[0]), b = __bfloat1622float2(p[1]);
+    const float2 c = __bfloat1622float2(p[2]), e = __bfloat1622float2(p[3]);
+    dst[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+    dst[2 * i + 1] = make_float4(c.x, c.y, e.x, e.y);
+  }
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// NV = float4 per lane (d = 128 * NV).  Row held in registers: one read of the fp32 row,
+// one write of the bf16 row.
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x,
+                                                      const float* __restrict__ g,
+                                                      __nv_bfloat16* __restrict__ y, int T,
+                                                      float eps) {
+  constexpr int d = NV * 128;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * d);
+  float4 v[NV];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = __ldcs(src + lane + 32 * i);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / (float)d + eps);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  uint2* dst = reinterpret_cast<uint2*>(y + (size_t)t * d);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float4 gg = __ldg(g4 + lane + 32 * i);
+    uint2 o;
+    o.x = pack_bf16x2(v[i].x * r * gg.x, v[i].y * r * gg.y);
+    o.y = pack_bf16x2(v[i].z * r * gg.z, v[i].w * r * gg.w);
+    dst[lane + 32 * i] = o;
+  }
+}
+
+// ---------------------------------------------------------------- last-token head
+// One warp per item: never forms [N x V] logits — only the yes/no columns of W_head are read.
+__global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ resid,
+                                                   const int32_t* __restrict__ last_idx,
+                                                   int n_items, int d,
+                                                   const float* __restrict__ g,
+                                                   const float* __restrict__ w_yes,
+                                                   const float* __restrict__ w_no, float eps,
+                                                   float* __restrict__ logits2,
+                                                   float* __restrict__ p_yes, int* bad) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n_items) return;
+  const float* x = resid + (size_t)__ldg(last_idx + i) * d;
+  float ss = 0.f;
+  for (int j = lane; j < d; j += 32) { const float v = x[j]; ss += v * v; }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / (float)d + eps);
+  float ly = 0.f, ln = 0.f;
+  for (int j = lane; j < d; j += 32) {
+    const float hn = x[j] * r * __ldg(g + j);
+    ly += hn * __ldg(w_yes + j);
+    ln += hn * __ldg(w_no + j);
+  }
+  ly = warp_sum(ly);
+  ln = warp_sum(ln);
+  if (lane == 0) {
+    logits2[2 * i] = ly;
+    logits2[2 * i + 1] = ln;
+    p_yes[i] = 1.f / (1.f + expf(-(ly - ln)));
+    if (!isfinite(ly) || !isfinite(ln)) atomicOr(bad, 1);
+  }
+}
+
+int launch_embed(const int32_t* ids, const void* emb, float* resid, int T, int d, int vocab,
+                 cudaStream_t stream) {
+  (void)vocab;
+  if (d % 8 != 0) return fail(-2, "embed: d_model must be a multiple of 8");
+  if (T == 0) return 0;
+  embed_kernel<<<(T + 7) / 8, 256, 0, stream>>>(ids, reinterpret_cast<const __nv_bfloat16*>(emb),
+                                                resid, T, d);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "embed launch: %s", cudaGetErrorString(e));
+}
+
+int launch_rmsnorm(const float* x, const float* g, void* y, int T, int d, float eps,
+                   cudaStream_t stream) {
+  if (T == 0) return 0;
+  const dim3 grid((T + 7) / 8);
+  auto* yb = reinterpret_cast<__nv_bfloat16*>(y);
+  switch (d) {
+    case 128: rmsnorm_kernel<1><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 256: rmsnorm_kernel<2><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 512: rmsnorm_kernel<4><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 768: rmsnorm_kernel<6><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 1024: rmsnorm_kernel<8><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 1536: rmsnorm_kernel<12><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 2048: rmsnorm_kernel<16><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 2560: rmsnorm_kernel<20><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 3072: rmsnorm_kernel<24><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    case 4096: rmsnorm_kernel<32><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    default: return fail(-2, "rmsnorm: unsupported d_model %d", d);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "rmsnorm launch: %s", cudaGetErrorString(e));
+}
+
+int launch_head(const float* resid, const int32_t* last_idx, int n_items, int d,
+                const float* g, const float* w_yes, const float* w_no, float eps, float* logits2,
+                float* p_yes, int* bad, cudaStream_t stream) {
+  if (n_items == 0) return 0;
+  head_kernel<<<(n_items + 7) / 8, 256, 0, stream>>>(resid, last_idx, n_items, d, g, w_yes, w_no,
+                                                     eps, logits2, p_yes, bad);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "head launch: %s", cudaGetErrorString(e));
+}
+
+}  // namespace pf

@@ -1,0 +1,353 @@
+// tcgen05 bf16 GEMM for the packed prefill:  C[M x N] = A[M x K] . B[N x K]^T
+//
+// A = activations (T packed tokens x K, row-major), B = weights stored K-major ([out x in], i.e.
+// the spec's x.W weights transposed at load).  Persistent, warp-specialised, 1 CTA per SM:
+//   warp 0      TMA producer (A 128x64 + B 256x64 bf16 boxes, 128B swizzle, STAGES-deep ring)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16 per op)
+//   warps 2..5  epilogue: tcgen05.ld -> fused op -> swizzled smem -> TMA store / TMA reduce-add
+// The accumulator is double-buffered in TMEM (2 x 256 fp32 columns) so the epilogue of tile i
+// overlaps the main loop of tile i+1.
+//
+// Fused epilogues:
+//   EPI_BF16       plain bf16 store
+//   EPI_ROPE_BF16  QKV projection: rotate-half RoPE on the first `rope_heads` 128-wide heads
+//   EPI_SWIGLU     gate/up projection with B rows interleaved per 128-neuron block
+//                  ([gate_j | up_j] per 256-row tile); writes silu(gate)*up as bf16 (N/2 cols)
+//   EPI_RESID_ADD  O / down projection: fp32 residual stream += acc via TMA reduce-add
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+#include "pf_internal.h"
+
+namespace pf {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BN = 256;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
+constexpr int GEMM_B_BYTES = GEMM_BN * GEMM_BK * 2;   // 32 KB
+constexpr int GEMM_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES;
+constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B staging box
+constexpr int GEMM_SMEM_BYTES =
+    1024 + GEMM_STAGES * GEMM_STAGE_BYTES + 4 * 2 * GEMM_STG_BYTES + 256;
+
+struct GemmArgs {
+  int M, N, K;
+  int num_m_blk, num_n_blk;
+  const int32_t* pos;      // EPI_ROPE: position per row
+  const float* rope_cos;   // [max_seq x 64]
+  const float* rope_sin;
+  int rope_heads;          // heads (of 128 cols) that receive RoPE
+};
+
+PF_DEVICE float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+// Write 32 packed words (one 128-byte row) into a 32x128B swizzled staging box.
+PF_DEVICE void stage_row_128B(uint32_t stg, uint32_t row, const uint32_t (&w)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint32_t addr = stg + row * 128 + ((c ^ (row & 7)) << 4);
+    st_shared_v4(addr, w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + GEMM_STAGES * GEMM_A_BYTES;
+  uint8_t* sStg = smem + GEMM_STAGES * GEMM_STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 2 * GEMM_STG_BYTES);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + GEMM_STAGES;
+  uint64_t* tfull_bar = bars + 2 * GEMM_STAGES;
+  uint64_t* tempty_bar = bars + 2 * GEMM_STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * GEMM_STAGES + 4);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int num_tiles = args.num_m_blk * args.num_n_blk;
+  const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    for (int s = 0; s < GEMM_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile / args.num_n_blk) * GEMM_BM;
+        const int n0 = (tile % args.num_n_blk) * GEMM_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], GEMM_STAGE_BYTES);
+          tma_load_2d(sA + stage * GEMM_A_BYTES, &tmA, &full_bar[stage], kb * GEMM_BK, m0);
+          tma_load_2d(sB + stage * GEMM_B_BYTES, &tmB, &full_bar[stage], kb * GEMM_BK, n0,
+                      kEvictLast);
+          if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, GEMM_BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * GEMM_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * GEMM_A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * GEMM_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            umma_bf16_ss(d_tmem, kmajor_desc(a_addr + k * 32), kmajor_desc(b_addr + k * 32), idesc,
+                         (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue (warps 2..5)
+    const uint32_t quad = warp & 3;          // TMEM lane quadrant this warp may access
+    const uint32_t row = quad * 32 + lane;   // row within the 128-row tile
+    uint8_t* my_stg = sStg + (warp - 2) * 2 * GEMM_STG_BYTES;
+    int stg_idx = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+
+    // Stage one 32x128B box and launch its TMA store / reduce. Buffers alternate; the wait
+    // keeps at most one store per warp in flight against the buffer being overwritten.
+    auto emit = [&](const uint32_t (&w)[32], int c0, int r0) {
+      if (lane == 0) tma_store_wait_read<1>();
+      __syncwarp();
+      const uint32_t stg = smem_u32(my_stg + stg_idx * GEMM_STG_BYTES);
+      stage_row_128B(stg, lane, w);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (EPI == EPI_RESID_ADD) tma_reduce_add_2d(&tmC, my_stg + stg_idx * GEMM_STG_BYTES, c0, r0);
+        else tma_store_2d(&tmC, my_stg + stg_idx * GEMM_STG_BYTES, c0, r0);
+        tma_store_commit();
+      }
+      stg_idx ^= 1;
+    };
+
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m0 = (tile / args.num_n_blk) * GEMM_BM;
+      const int n0 = (tile % args.num_n_blk) * GEMM_BN;
+      const int r0 = m0 + quad * 32;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * GEMM_BN;
+
+      if constexpr (EPI == EPI_BF16) {
+#pragma unroll 1
+        for (int c = 0; c < GEMM_BN / 64; ++c) {
+          uint32_t v0[32], v1[32], w[32];
+          tmem_ld_32x32b_x32(t_row + c * 64, v0);
+          tmem_ld_32x32b_x32(t_row + c * 64 + 32, v1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w[i] = pack_bf16x2(__uint_as_float(v0[2 * i]), __uint_as_float(v0[2 * i + 1]));
+            w[16 + i] = pack_bf16x2(__uint_as_float(v1[2 * i]), __uint_as_float(v1[2 * i + 1]));
+          }
+          emit(w, n0 + c * 64, r0);
+        }
+      } else if constexpr (EPI == EPI_RESID_ADD) {
+#pragma unroll 1
+        for (int c = 0; c < GEMM_BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, v);
+          tmem_ld_wait();
+          emit(v, n0 + c * 32, r0);
+        }
+      } else if constexpr (EPI == EPI_SWIGLU) {
+        // B tile rows [0,128) = gate neurons, [128,256) = matching up neurons.
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t w[32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t g[32], u[32];
+            tmem_ld_32x32b_x32(t_row + c * 64 + h * 32, g);
+            tmem_ld_32x32b_x32(t_row + 128 + c * 64 + h * 32, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+              float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+              w[h * 16 + i] = pack_bf16x2(a0, a1);
+            }
+          }
+          emit(w, n0 / 2 + c * 64, r0);
+        }
+      } else {  // EPI_ROPE_BF16
+        // Rotate-half RoPE: head column i pairs with i+64.  For each 32-column half c the thread
+        // loads x1 = cols [32c, 32c+32) and x2 = cols [64+32c, ...); rotated x1 lands in the
+        // "lo" 64-col box (16-byte chunks 4c..4c+3), rotated x2 in the "hi" box.
+        const int grow = m0 + row;
+        const int p = (grow < args.M) ? __ldg(args.pos + grow) : 0;
+        const float4* cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * 64);
+        const float4* sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * 64);
+        const uint32_t stg_lo = smem_u32(my_stg);
+        const uint32_t stg_hi = smem_u32(my_stg + GEMM_STG_BYTES);
+#pragma unroll 1
+        for (int hd = 0; hd < GEMM_BN / 128; ++hd) {
+          const bool rot = ((n0 + hd * 128) / 128) < args.rope_heads;
+          if (lane == 0) tma_store_wait_read<0>();
+          __syncwarp();
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            uint32_t x1[32], x2[32];
+            tmem_ld_32x32b_x32(t_row + hd * 128 + c * 32, x1);
+            tmem_ld_32x32b_x32(t_row + hd * 128 + 64 + c * 32, x2);
+            tmem_ld_wait();
+            uint32_t w1[16], w2[16];
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              float4 cv = make_float4(1.f, 1.f, 1.f, 1.f), sv = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (rot) { cv = __ldg(cs4 + c * 8 + j4); sv = __ldg(sn4 + c * 8 + j4); }
+              const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
+              const float ss[4] = {sv.x, sv.y, sv.z, sv.w};
+              float o1[4], o2[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float a = __uint_as_float(x1[j4 * 4 + e]);
+                const float b = __uint_as_float(x2[j4 * 4 + e]);
+                o1[e] = a * cc[e] - b * ss[e];
+                o2[e] = b * cc[e] + a * ss[e];
+              }
+              w1[j4 * 2] = pack_bf16x2(o1[0], o1[1]);
+              w1[j4 * 2 + 1] = pack_bf16x2(o1[2], o1[3]);
+              w2[j4 * 2] = pack_bf16x2(o2[0], o2[1]);
+              w2[j4 * 2 + 1] = pack_bf16x2(o2[2], o2[3]);
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const uint32_t off = lane * 128 + (((c * 4 + q4) ^ (lane & 7)) << 4);
+              st_shared_v4(stg_lo + off, w1[4 * q4], w1[4 * q4 + 1], w1[4 * q4 + 2], w1[4 * q4 + 3]);
+              st_shared_v4(stg_hi + off, w2[4 * q4], w2[4 * q4 + 1], w2[4 * q4 + 2], w2[4 * q4 + 3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, my_stg, n0 + hd * 128, r0);
+            tma_store_2d(&tmC, my_stg + GEMM_STG_BYTES, n0 + hd * 128 + 64, r0);
+            tma_store_commit();
+          }
+        }
+      }
+      // All TMEM reads of this accumulator are complete (tcgen05.wait::ld above).
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+
+int gemm_smem_bytes() { return GEMM_SMEM_BYTES; }
+
+static int g_num_sms = 0;
+
+template <int EPI>
+static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                         const GemmArgs& a, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES);
+    if (e != cudaSuccess) return fail(-4, "gemm smem attr: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  const int tiles = a.num_m_blk * a.num_n_blk;
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  gemm_bf16_kernel<EPI><<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(ta, tb, tc, a);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "gemm launch: %s", cudaGetErrorString(e));
+}
+
+int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t stream) {
+  if (d.M == 0) return 0;
+  if (d.K % 64 != 0) return fail(-2, "gemm: K=%d must be a multiple of 64", d.K);
+  if (d.N % 128 != 0) return fail(-2, "gemm: N=%d must be a multiple of 128", d.N);
+  if (d.epilogue == EPI_SWIGLU && d.N % GEMM_BN != 0)
+    return fail(-2, "gemm: SwiGLU N=%d must be a multiple of %d", d.N, GEMM_BN);
+  if (d.epilogue == EPI_ROPE_BF16 && (d.pos == nullptr || d.rope_cos == nullptr))
+    return fail(-2, "gemm: RoPE epilogue needs positions and tables");
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  CUtensorMap ta, tb, tc;
+  if (!make_tmap_2d(&ta, d.A, 2, d.M, d.K, d.lda, GEMM_BM, GEMM_BK, true)) return -3;
+  if (cached_b) tb = *cached_b;
+  else if (!make_tmap_2d(&tb, d.B, 2, d.N, d.K, d.ldb, GEMM_BN, GEMM_BK, true)) return -3;
+  const int out_cols = d.epilogue == EPI_SWIGLU ? d.N / 2 : d.N;
+  if (d.epilogue == EPI_RESID_ADD) {
+    if (!make_tmap_2d(&tc, d.C, 4, d.M, out_cols, d.ldc, 32, 32, true)) return -3;
+  } else {
+    if (!make_tmap_2d(&tc, d.C, 2, d.M, out_cols, d.ldc, 32, 64, true)) return -3;
+  }
+  GemmArgs a;
+  a.M = d.M; a.N = d.N; a.K = d.K;
+  a.num_m_blk = (d.M + GEMM_BM - 1) / GEMM_BM;
+  a.num_n_blk = (d.N + GEMM_BN - 1) / GEMM_BN;
+  a.pos = d.pos; a.rope_cos = d.rope_cos; a.rope_sin = d.rope_sin; a.rope_heads = d.rope_heads;
+  switch (d.epilogue) {
+    case EPI_BF16: return launch_gemm_t<EPI_BF16>(ta, tb, tc, a, stream);
+    case EPI_ROPE_BF16: return launch_gemm_t<EPI_ROPE_BF16>(ta, tb, tc, a, stream);
+    case EPI_SWIGLU: return launch_gemm_t<EPI_SWIGLU>(ta, tb, tc, a, stream);
+    case EPI_RESID_ADD: return launch_gemm_t<EPI_RESID_ADD>(ta, tb, tc, a, stream);
+    default: return fail(-2, "gemm: unknown epilogue %d", d.epilogue);
+  }
+}
+
+}  // namespace pf

@@ -1,0 +1,65 @@
+// Internal declarations shared by the CUDA translation units of libprefill_sm100.so.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace pf {
+
+enum Epilogue : int {
+  EPI_BF16 = 0,
+  EPI_ROPE_BF16 = 1,
+  EPI_SWIGLU = 2,
+  EPI_RESID_ADD = 3,
+};
+
+// ---- error state (thread-local message, negative return codes; see include/prefill_sm100.h)
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+
+// ---- tensor maps (host)
+// 2-D row-major tensor [rows x cols] of `elem_bytes`-sized elements, `ld` elements per row,
+// box = [box_rows x box_cols], 128-byte swizzle when box_cols*elem_bytes == 128.
+bool make_tmap_2d(CUtensorMap* out, const void* base, int elem_bytes, uint64_t rows, uint64_t cols,
+                  uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+
+// ---- launchers (return 0 or negative error code)
+struct GemmDesc {
+  const void* A;     // [M x K] bf16, leading dim lda
+  int lda;
+  const void* B;     // [N x K] bf16, leading dim ldb
+  int ldb;
+  void* C;           // bf16 [M x ldc] (fp32 for EPI_RESID_ADD)
+  int ldc;
+  int M, N, K;
+  int epilogue;
+  const int32_t* pos;
+  const float* rope_cos;
+  const float* rope_sin;
+  int rope_heads;
+  int max_seq;
+};
+int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t stream);
+int gemm_smem_bytes();
+
+int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, int T, int d, int vocab,
+                 cudaStream_t stream);
+int launch_rmsnorm(const float* resid, const float* gamma, void* out_bf16, int T, int d, float eps,
+                   cudaStream_t stream);
+int launch_head(const float* resid, const int32_t* last_idx, int n_items, int d,
+                const float* final_gamma, const float* w_yes, const float* w_no, float eps,
+                float* logits2, float* p_yes, int* bad_flag, cudaStream_t stream);
+
+struct AttnDesc {
+  const void* qkv;        // [T x (H+2Hkv)*dh] bf16 (RoPE already applied to q, k)
+  void* out;              // [T x H*dh] bf16
+  int T, H, Hkv, dh;
+  const int32_t* work;    // [n_work x 4] : {seg_kind|qtile, q_row0, q_rows, seg_index}
+  int n_work;
+  const int32_t* segs;    // [n_seg x 4] : {prefix_off, P, suffix_off, S}  (prefix segment: S=0)
+  float scale;
+};
+int launch_attention(const AttnDesc& d, cudaStream_t stream);
+
+}  // namespace pf

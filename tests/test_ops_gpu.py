@@ -1,0 +1,190 @@
+"""Op-level numerics of the sm_100a kernels against plain PyTorch fp32 references.
+
+Every call goes through the C-ABI (libprefill_sm100.so via ctypes).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2510_22101_b200 import _lib  # noqa: E402
+from paper_2510_22101_b200.config import ModelConfig  # noqa: E402
+from paper_2510_22101_b200.prefixcache import SharedBatch, pack_requests  # noqa: E402
+from paper_2510_22101_b200.weights import interleave_gate_up, rope_tables  # noqa: E402
+
+
+def P(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return _lib.load()
+
+
+def gemm(lib, A, B, C, epi, pos=None, cos=None, sin=None, rope_heads=0):
+    M, K = A.shape
+    N = B.shape[0]
+    rc = lib.pf_gemm_bf16(P(A), A.stride(0), P(B), B.stride(0), P(C), C.stride(0), M, N, K, epi,
+                          P(pos), P(cos), P(sin), rope_heads, stream())
+    _lib.check(rc)
+    torch.cuda.synchronize()
+
+
+def rand_bf16(*shape, scale=1.0, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(*shape, generator=g, device="cuda") * scale).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 512, 256), (128, 256, 64), (8192, 1024, 512),
+                                   (333, 2560, 2048)])
+def test_gemm_bf16(lib, M, N, K):
+    A = rand_bf16(M, K, seed=1)
+    B = rand_bf16(N, K, scale=K ** -0.5, seed=2)
+    C = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    gemm(lib, A, B, C, _lib.EPI_BF16)
+    ref = A.float() @ B.float().t()
+    torch.testing.assert_close(C.float(), ref, rtol=1.6e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 256, 128), (5000, 2048, 1280)])
+def test_gemm_resid_add(lib, M, N, K):
+    A = rand_bf16(M, K, seed=3)
+    B = rand_bf16(N, K, scale=K ** -0.5, seed=4)
+    C0 = torch.randn(M, N, device="cuda")
+    C = C0.clone()
+    gemm(lib, A, B, C, _lib.EPI_RESID_ADD)
+    ref = C0 + A.float() @ B.float().t()
+    torch.testing.assert_close(C, ref, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("M,F,K", [(700, 384, 256), (3000, 3712, 2048)])
+def test_gemm_swiglu(lib, M, F, K):
+    A = rand_bf16(M, K, seed=5)
+    G = rand_bf16(F, K, scale=K ** -0.5, seed=6)
+    U = rand_bf16(F, K, scale=K ** -0.5, seed=7)
+    Fp = -(-F // 128) * 128
+    if Fp % 256:  # the SwiGLU tile covers 2 neuron blocks... keep F_pad a multiple of 128
+        pass
+    B = interleave_gate_up(G, U, Fp).contiguous()
+    if B.shape[0] % 256:
+        pytest.skip("SwiGLU GEMM needs 2*F_pad % 256 == 0")
+    C = torch.full((M, Fp), float("nan"), device="cuda", dtype=torch.bfloat16)
+    gemm(lib, A, B, C, _lib.EPI_SWIGLU)
+    g = A.float() @ G.float().t()
+    u = A.float() @ U.float().t()
+    ref = torch.nn.functional.silu(g) * u
+    torch.testing.assert_close(C[:, :F].float(), ref, rtol=2e-2, atol=2e-2)
+
+
+def rope_ref(x, pos, cos, sin, n_rot_heads, dh=128):
+    x = x.clone()
+    c = cos[pos.long()]  # [M, dh/2]
+    s = sin[pos.long()]
+    for h in range(n_rot_heads):
+        a = x[:, h * dh: h * dh + dh // 2].clone()
+        b = x[:, h * dh + dh // 2: (h + 1) * dh].clone()
+        x[:, h * dh: h * dh + dh // 2] = a * c - b * s
+        x[:, h * dh + dh // 2: (h + 1) * dh] = b * c + a * s
+    return x
+
+
+@pytest.mark.parametrize("M,H,Hkv,K", [(900, 2, 1, 256), (2000, 10, 5, 2048)])
+def test_gemm_rope(lib, M, H, Hkv, K):
+    cfg = ModelConfig(n_layers=1, d_model=K, n_heads=H, n_kv_heads=Hkv, d_ff=128, d_head=128)
+    cos, sin = (torch.from_numpy(t).cuda() for t in rope_tables(cfg))
+    N = (H + 2 * Hkv) * 128
+    A = rand_bf16(M, K, seed=8)
+    B = rand_bf16(N, K, scale=K ** -0.5, seed=9)
+    pos = torch.randint(0, cfg.max_seq, (M,), device="cuda", dtype=torch.int32)
+    C = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    gemm(lib, A, B, C, _lib.EPI_ROPE_BF16, pos, cos, sin, H + Hkv)
+    ref = rope_ref(A.float() @ B.float().t(), pos, cos, sin, H + Hkv)
+    torch.testing.assert_close(C.float(), ref, rtol=1.6e-2, atol=2e-2)
+
+
+def attention_ref(qkv, packed, H, Hkv, dh=128):
+    T = qkv.shape[0]
+    q = qkv[:, : H * dh].float().view(T, H, dh)
+    k = qkv[:, H * dh: (H + Hkv) * dh].float().view(T, Hkv, dh)
+    v = qkv[:, (H + Hkv) * dh:].float().view(T, Hkv, dh)
+    out = torch.zeros(T, H, dh, device=qkv.device)
+    grp = H // Hkv
+    for kv_off, kv_len, q_off, q_len in packed.segs.tolist():
+        rows = torch.arange(q_off, q_off + q_len, device=qkv.device)
+        keys = torch.cat([torch.arange(kv_off, kv_off + kv_len, device=qkv.device), rows])
+        kk = k[keys].repeat_interleave(grp, dim=1)  # [nk, H, dh]
+        vv = v[keys].repeat_interleave(grp, dim=1)
+        s = torch.einsum("qhd,khd->hqk", q[rows], kk) / dh ** 0.5
+        mask = torch.ones(q_len, kv_len + q_len, dtype=torch.bool, device=qkv.device)
+        mask[:, kv_len:] = torch.tril(torch.ones(q_len, q_len, dtype=torch.bool, device=qkv.device))
+        s = s.masked_fill(~mask, float("-inf"))
+        out[rows] = torch.einsum("hqk,khd->qhd", torch.softmax(s, dim=-1), vv)
+    return out.view(T, H * dh)
+
+
+@pytest.mark.parametrize("H,Hkv", [(2, 1), (4, 2), (10, 5)])
+def test_prefix_attention(lib, H, Hkv):
+    rng = np.random.default_rng(0)
+    reqs = [
+        SharedBatch(list(rng.integers(16, 100, 64)), [list(rng.integers(16, 100, s)) for s in (100, 128, 200, 1, 300)]),
+        SharedBatch(list(rng.integers(16, 100, 5)), [list(rng.integers(16, 100, 130))]),
+        SharedBatch([], [list(rng.integers(16, 100, 7)), list(rng.integers(16, 100, 129))]),
+        SharedBatch(list(rng.integers(16, 100, 200)), [list(rng.integers(16, 100, 3))]),
+    ]
+    packed = pack_requests(reqs)
+    T = packed.T
+    qkv = rand_bf16(T, (H + 2 * Hkv) * 128, seed=11)
+    out = torch.full((T, H * 128), float("nan"), device="cuda", dtype=torch.bfloat16)
+    segs = torch.from_numpy(packed.segs).cuda()
+    work = torch.from_numpy(packed.work).cuda()
+    rc = lib.pf_prefix_attention(P(qkv), P(out), T, H, Hkv, 128, P(segs), P(work), len(packed.work), stream())
+    _lib.check(rc)
+    torch.cuda.synchronize()
+    ref = attention_ref(qkv, packed, H, Hkv)
+    torch.testing.assert_close(out.float(), ref, rtol=2e-2, atol=2e-2)
+
+
+def test_embed_rmsnorm_head(lib):
+    T, d, V = 777, 2048, 1000
+    emb = rand_bf16(V, d, seed=12)
+    ids = torch.randint(0, V, (T,), device="cuda", dtype=torch.int32)
+    resid = torch.empty(T, d, device="cuda")
+    _lib.check(lib.pf_embed(P(ids), P(emb), P(resid), T, d, stream()))
+    torch.cuda.synchronize()
+    torch.testing.assert_close(resid, emb[ids.long()].float(), rtol=0, atol=0)
+
+    x = torch.randn(T, d, device="cuda") * 3
+    g = torch.rand(d, device="cuda") + 0.5
+    y = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    _lib.check(lib.pf_rmsnorm(P(x), P(g), P(y), T, d, ctypes.c_float(1e-6), stream()))
+    torch.cuda.synchronize()
+    ref = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-6) * g
+    torch.testing.assert_close(y.float(), ref, rtol=1e-2, atol=1e-2)
+
+    n = 50
+    last = torch.randint(0, T, (n,), device="cuda", dtype=torch.int32)
+    wy = torch.randn(d, device="cuda") / d ** 0.5
+    wn = torch.randn(d, device="cuda") / d ** 0.5
+    logits2 = torch.empty(n, 2, device="cuda")
+    p = torch.empty(n, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(lib.pf_head_last_token(P(x), P(last), n, d, P(g), P(wy), P(wn), ctypes.c_float(1e-6),
+                                      P(logits2), P(p), P(bad), stream()))
+    torch.cuda.synchronize()
+    h = x[last.long()]
+    hn = h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + 1e-6) * g
+    ly, ln = hn @ wy, hn @ wn
+    torch.testing.assert_close(logits2[:, 0], ly, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(logits2[:, 1], ln, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(p, torch.sigmoid(ly - ln), rtol=1e-5, atol=1e-5)
+    assert int(bad.item()) == 0
