@@ -1,0 +1,350 @@
+"""Throughput benchmark of the B200 prefill scoring path (contract: see DESIGN.md §6).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C4] [--impl ours|reference]
+
+One step = one packed scoring pass (pf_score) over one synthetic request per GPU: a 64-token
+query prefix shared by the config's items (C4: 256 items x 100 tokens).  N > 1 runs under
+torchrun as independent replicas (one process per GPU, no collective on the data path; the
+timing is max-over-ranks via one all_reduce after the timed region).
+
+`value`  items/s with inputs resident in HBM (CUDA events around K back-to-back pf_score calls).
+`e2e`    the same through pf_score_host: pinned host buffers -> H2D -> forward -> D2H -> sync.
+`roofline` the dominant kernel (gate/up SwiGLU tcgen05 GEMM) timed alone with CUDA events.
+`cpu_baseline` the numpy fp32 oracle (oracle/, "port") on a bounded item sample, rank 0, N=1.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "items scored/sec & prefill tok/s per B200 (1/2/4/8 GPUs), % bf16 TC peak; p99 ms"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def algorithmic_flops(cfg, prefix_len, suffix_lens) -> float:
+    """L*[(P + sum S) * linear_flops/token + 4*H*dh*(sum_{t<=P} t + sum_i sum_t (P+t))]
+    at true (unpadded) widths; prefix counted once; causal attention over unmasked pairs."""
+    P = prefix_len
+    S = np.asarray(suffix_lens, dtype=np.float64)
+    tokens = P + S.sum()
+    attn_pairs = P * (P + 1) / 2 + np.sum(S * P + S * (S + 1) / 2)
+    return cfg.n_layers * (tokens * cfg.linear_flops_per_token() + 4 * cfg.n_heads * cfg.d_head * attn_pairs)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpus):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", ",".join(map(str, gpus)), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1])); smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def make_request(cfg, shape, seed):
+    from paper_2510_22101_b200 import pack_requests, split_shared_prefix
+
+    rng = np.random.default_rng(seed)
+    prefix = [3] + [int(x) for x in rng.integers(16, cfg.vocab_size, shape.prefix_len - 1)]
+    prompts = []
+    for _ in range(shape.n_items):
+        suf = [int(x) for x in rng.integers(16, cfg.vocab_size, shape.suffix_len)]
+        suf[-1] = 11  # <|ans|>, Eq 1
+        prompts.append(prefix + suf)
+    sbs = [split_shared_prefix(prompts) for _ in range(shape.n_requests)]
+    return sbs, pack_requests(sbs, cfg.max_seq)
+
+
+def cpu_oracle_sample(cfg, sbs, budget_s: float, max_items: int):
+    """Time the numpy fp32 oracle's score_shared_batch on a bounded item sample."""
+    import oracle.model as OM
+    import oracle.prefixcache as OP
+
+    ow = OM.init_weights(cfg, 0)
+    sb = sbs[0]
+    # calibrate with one item
+    t0 = time.perf_counter()
+    OP.score_shared_batch(ow, OP.SharedBatch(sb.prefix_tokens, sb.suffixes[:1]))
+    t_one = time.perf_counter() - t0
+    n = int(max(2, min(max_items, budget_s / max(t_one, 1e-6))))
+    t0 = time.perf_counter()
+    OP.score_shared_batch(ow, OP.SharedBatch(sb.prefix_tokens, sb.suffixes[:n]))
+    dt = time.perf_counter() - t0
+    toks = len(sb.prefix_tokens) + sum(len(s) for s in sb.suffixes[:n])
+    return {"value": n / dt, "unit": "items/s", "cores": blas_threads(), "kind": "port",
+            "sample": f"oracle score_shared_batch (numpy fp32): prefix {len(sb.prefix_tokens)} + "
+                      f"{n} of {len(sb.suffixes)} items ({toks} tokens) in {dt:.1f} s",
+            "tok_per_s": toks / dt}
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_config(name, cfg, shape, n_gpus):
+    return {
+        "workload": (f"{name}: L{cfg.n_layers} d{cfg.d_model} {cfg.n_heads}q/{cfg.n_kv_heads}kv "
+                     f"dh{cfg.d_head} d_ff{cfg.d_ff}; prefix {shape.prefix_len} shared by "
+                     f"{shape.n_items} items x {shape.suffix_len} tokens per GPU per step"),
+        "items_per_gpu_step": shape.n_items * shape.n_requests,
+        "tokens_per_gpu_step": shape.tokens,
+        "prefix_len": shape.prefix_len, "suffix_len": shape.suffix_len,
+        "parallelism": f"replicas x{n_gpus} (request-sharded, no collective)",
+        "l2": "working set > L2 (weights + activations stream every step)",
+    }
+
+
+def run_reference(args):
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return
+    from paper_2510_22101_b200 import CONFIGS, REQUESTS
+
+    cfg, shape = CONFIGS[args.config], REQUESTS[args.config]
+    import oracle.model as OM
+    import oracle.prefixcache as OP
+
+    sbs, _ = make_request(cfg, shape, seed=1000)
+    ow = OM.init_weights(cfg, 0)
+    sb = sbs[0]
+    m = args.ref_items
+    step = lambda i: OP.score_shared_batch(
+        ow, OP.SharedBatch(sb.prefix_tokens, sb.suffixes[(i * m) % shape.n_items:][:m]))
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    dt = time.perf_counter() - t0
+    value = args.steps * m / dt
+    toks = len(sb.prefix_tokens) + m * shape.suffix_len
+    line = {
+        "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded uniform token ids, <|ans|> last token; random-init bf16-valued weights)",
+        "config": workload_config(args.config, cfg, shape, ws),
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "items/s", "cores": blas_threads(), "kind": "port",
+                         "sample": f"per step: oracle score_shared_batch, prefix {len(sb.prefix_tokens)} + "
+                                   f"{m} items ({toks} tokens), numpy fp32 on host cores"},
+        "e2e": {"value": value, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "tok_per_s": args.steps * toks / dt,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_22101_b200 import CONFIGS, REQUESTS, _lib, init_device_weights
+    from paper_2510_22101_b200.engine import DevicePacked, PinnedPacked, PrefillScorer
+
+    ws, rank, local = dist_info()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg, shape = CONFIGS[args.config], REQUESTS[args.config]
+    peak_burst, peak_sust, hbm, peak_kind = load_peaks()
+
+    weights = init_device_weights(cfg, seed=0, device=dev)
+    scorer = PrefillScorer(weights, device=dev)
+    sbs, packed = make_request(cfg, shape, seed=1000 + rank)
+    dp = DevicePacked(packed, dev)
+    pp = PinnedPacked(packed)
+    n_items = packed.n_items
+    flops_step = algorithmic_flops(cfg, shape.prefix_len, [shape.suffix_len] * shape.n_items) * shape.n_requests
+    launches_per_step = 2 + 7 * cfg.n_layers
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    logits2 = torch.empty((n_items, 2), dtype=torch.float32, device=dev)
+    p_yes = torch.empty((n_items,), dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        scorer.score_device(dp, logits2, p_yes)
+    torch.cuda.synchronize()
+    if int(scorer._bad[0].item()) != 0:
+        raise RuntimeError("non-finite logits in warm-up")
+
+    clocks = ClockSampler([local] if ws == 1 else list(range(ws))) if rank == 0 else None
+    # ---------------------------------------------------------------- device-resident timing
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        scorer.score_device(dp, logits2, p_yes, check=False)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    # ---------------------------------------------------------------- end-to-end (host buffers)
+    for _ in range(2):
+        scorer.score_host(pp)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        scorer.score_host(pp)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    clk = clocks.stop() if clocks else None
+
+    # ---------------------------------------------------------------- dominant kernel alone
+    lib = _lib.load()
+    T, d = packed.T, cfg.d_model
+    A = (torch.randn(T, d, device=dev) * 0.5).to(torch.bfloat16)
+    C = torch.empty(T, cfg.d_ff_pad, device=dev, dtype=torch.bfloat16)
+    B = weights.w_gu[0]
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    gemm = lambda: _lib.check(lib.pf_gemm_bf16(A.data_ptr(), d, B.data_ptr(), d, C.data_ptr(), cfg.d_ff_pad,
+                                               T, 2 * cfg.d_ff_pad, d, _lib.EPI_SWIGLU, None, None, None, 0, sp))
+    for _ in range(3):
+        gemm()
+    reps = 20
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(reps):
+        gemm()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = ev0.elapsed_time(ev1) / reps
+    k_flops = 2.0 * T * d * 2 * cfg.d_ff
+    achieved = k_flops / (k_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.config, {}).get("gate_up_gemm_dram_bytes")
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(cfg, sbs, args.cpu_seconds, shape.n_items)
+
+    ms_step = dev_ms / args.steps
+    items_total = n_items * ws
+    value = items_total / (ms_step * 1e-3)
+    e2e_val = items_total * args.steps / e2e_s
+    line = {
+        "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded uniform token ids, <|ans|> last token; random-init bf16 weights)",
+        "config": workload_config(args.config, cfg, shape, ws),
+        "tok_per_s": packed.T * ws / (ms_step * 1e-3),
+        "step_tensor_frac": {"achieved_tflops": flops_step / (ms_step * 1e-3) / 1e12,
+                             "frac_of_sustained": flops_step / (ms_step * 1e-3) / 1e12 / peak_sust,
+                             "frac_of_burst": flops_step / (ms_step * 1e-3) / 1e12 / peak_burst,
+                             "peak_kind": peak_kind},
+        "e2e": {"value": e2e_val, "unit": "items/s", "h2d_bytes_per_step": pp.h2d_bytes(),
+                "d2h_bytes_per_step": pp.d2h_bytes(), "ms_per_step": e2e_s / args.steps * 1e3},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"kernel": "gemm_bf16_kernel<EPI_SWIGLU> (gate/up)", "bound": "tensor",
+                     "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
+                     "frac": achieved / peak_burst, "traffic": traffic,
+                     "flops_per_launch": k_flops, "ms_per_launch": k_ms, "peak_kind": peak_kind},
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-items", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -121,17 +121,14 @@ int launch_rmsnorm(const float* x, const float* g, void* y, int T, int d, float 
   if (T == 0) return 0;
   const dim3 grid((T + 7) / 8);
   auto* yb = reinterpret_cast<__nv_bfloat16*>(y);
-  switch (d) {
-    case 128: rmsnorm_kernel<1><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 256: rmsnorm_kernel<2><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 512: rmsnorm_kernel<4><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 768: rmsnorm_kernel<6><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 1024: rmsnorm_kernel<8><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 1536: rmsnorm_kernel<12><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 2048: rmsnorm_kernel<16><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 2560: rmsnorm_kernel<20><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 3072: rmsnorm_kernel<24><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
-    case 4096: rmsnorm_kernel<32><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+  if (d % 128 != 0 || d < 128 || d > 4096) return fail(-2, "rmsnorm: unsupported d_model %d", d);
+  switch (d / 128) {
+#define PF_RMS_CASE(n) case n: rmsnorm_kernel<n><<<grid, 256, 0, stream>>>(x, g, yb, T, eps); break;
+    PF_RMS_CASE(1) PF_RMS_CASE(2) PF_RMS_CASE(3) PF_RMS_CASE(4) PF_RMS_CASE(5) PF_RMS_CASE(6)
+    PF_RMS_CASE(7) PF_RMS_CASE(8) PF_RMS_CASE(9) PF_RMS_CASE(10) PF_RMS_CASE(11) PF_RMS_CASE(12)
+    PF_RMS_CASE(13) PF_RMS_CASE(14) PF_RMS_CASE(15) PF_RMS_CASE(16) PF_RMS_CASE(18) PF_RMS_CASE(20)
+    PF_RMS_CASE(24) PF_RMS_CASE(28) PF_RMS_CASE(32)
+#undef PF_RMS_CASE
     default: return fail(-2, "rmsnorm: unsupported d_model %d", d);
   }
   cudaError_t e = cudaGetLastError();

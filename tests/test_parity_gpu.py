@@ -1,0 +1,132 @@
+"""End-to-end parity of the B200 scoring path against the CPU fp32 oracle.
+
+Gates:
+  * |Δp_yes| <= 1e-2 per item (the tolerance north_star states; written here);
+  * per-request top-10 identical under rank_items rules, modulo declared near-ties (oracle gap
+    < 2 max|Δp|; counted and printed).  Template family (every suffix ends in <|ans|>): random-init
+    scores cluster, many near-ties.  Spread family (random last token): few or none.
+Weights: init_weights(cfg, seed) — the same bf16-representable values on both sides.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import oracle.model as OM  # noqa: E402
+import oracle.prefixcache as OP  # noqa: E402
+import oracle.scoring as OS  # noqa: E402
+from paper_2510_22101_b200 import CONFIGS, init_weights, pack_requests  # noqa: E402
+from paper_2510_22101_b200.engine import PrefillScorer, score_shared_batch  # noqa: E402
+from tests.synth import make_shared  # noqa: E402
+
+TOL_P = 1e-2
+TOP_K = 10
+
+
+def oracle_scores(ow, batches):
+    out = []
+    for sb in batches:
+        osb = OP.SharedBatch(list(sb.prefix_tokens), [list(s) for s in sb.suffixes])
+        for logits in OP.score_shared_batch(ow, osb):
+            out.append(OS.relevance_score(logits)[0])
+    return np.asarray(out)
+
+
+def check_request_topk(p_ref, p_gpu, family, max_dp):
+    """Top-10 identical; oracle pairs closer than 2 max|dp| are declared near-ties (bf16 vs fp32
+    activations cannot order them) and counted.  Outside near-ties the order must match exactly."""
+    gap = 2 * max_dp
+    assert OS.topk_equal_modulo_ties(p_ref, p_gpu, TOP_K, gap)
+    ties = OS.near_tie_pairs(p_ref, TOP_K, gap)
+    if ties == 0:
+        assert OS.rank_items(p_ref)[:TOP_K] == OS.rank_items(p_gpu)[:TOP_K]
+    return ties
+
+
+_models = {}
+
+
+def get_models(name, seed=0):
+    if name not in _models:
+        cfg = CONFIGS[name]
+        _models[name] = (cfg, PrefillScorer(init_weights(cfg, seed)), OM.init_weights(cfg, seed))
+    return _models[name]
+
+
+@pytest.mark.parametrize("name", ["TINY", "TINY_GQA"])
+@pytest.mark.parametrize("family", ["template", "spread"])
+def test_model_parity_small(name, family):
+    cfg, scorer, ow = get_models(name)
+    rng = np.random.default_rng(1234)
+    batches = [
+        make_shared(rng, 64, [128] * 32, family),                       # C1-shaped request
+        make_shared(rng, 20, list(rng.integers(1, 300, 24)), family),   # ragged suffixes
+        make_shared(rng, 200, [1, 2, 129, 257], family),                # long prefix, tiny items
+    ]
+    assert len(batches[0].prefix_tokens) == 64
+    res = score_shared_batch(scorer, batches)
+    p_ref = oracle_scores(ow, batches)
+    dp = np.abs(res.p_yes.astype(np.float64) - p_ref)
+    max_dp = float(dp.max())
+    print(f"{name}/{family}: max|dp|={max_dp:.2e} mean={dp.mean():.2e}")
+    assert max_dp <= TOL_P
+    off = 0
+    ties = 0
+    for sb in batches:
+        n = sb.n_items
+        ties += check_request_topk(p_ref[off:off + n], res.p_yes[off:off + n], family, max_dp)
+        off += n
+    print(f"near-ties declared: {ties}")
+
+
+def test_single_item_and_no_prefix():
+    """Degenerate batches: batch of 1 and empty common prefix."""
+    cfg, scorer, ow = get_models("TINY")
+    rng = np.random.default_rng(7)
+    one = make_shared(rng, 0, [50], "spread")        # batch of 1 -> prefix = all but last token
+    assert len(one.prefix_tokens) == 49 and len(one.suffixes[0]) == 1
+    nop = OP.split_shared_prefix([[5, 6, 7], [8, 9]])
+    from paper_2510_22101_b200.prefixcache import SharedBatch
+    nop = SharedBatch(nop.prefix_tokens, nop.suffixes)
+    res = score_shared_batch(scorer, [one, nop])
+    p_ref = oracle_scores(ow, [one, nop])
+    assert np.max(np.abs(res.p_yes - p_ref)) <= TOL_P
+
+
+def test_packed_equals_separate_calls():
+    """Packing several requests into one launch gives the same scores as one launch each."""
+    cfg, scorer, _ = get_models("TINY_GQA")
+    rng = np.random.default_rng(3)
+    batches = [make_shared(rng, 30, list(rng.integers(1, 200, 9)), "spread") for _ in range(3)]
+    joint = score_shared_batch(scorer, batches).p_yes
+    sep = np.concatenate([score_shared_batch(scorer, b).p_yes for b in batches])
+    np.testing.assert_allclose(joint, sep, rtol=0, atol=1e-6)
+
+
+def test_host_path_matches_device_path():
+    from paper_2510_22101_b200.engine import PinnedPacked
+
+    cfg, scorer, _ = get_models("TINY")
+    rng = np.random.default_rng(5)
+    packed = pack_requests([make_shared(rng, 64, [100] * 16, "spread")])
+    dev = scorer.score_packed(packed)
+    host = scorer.score_host(PinnedPacked(packed))
+    np.testing.assert_array_equal(dev.p_yes, host.p_yes)
+    np.testing.assert_array_equal(dev.logits2, host.logits2)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,P,S,n", [("C4", 64, 100, 8), ("C2", 64, 128, 6)])
+def test_model_parity_full_size(name, P, S, n):
+    """Headline shapes (28 layers) on a bounded item sample the CPU oracle finishes quickly."""
+    cfg, scorer, ow = get_models(name)
+    rng = np.random.default_rng(11)
+    batches = [make_shared(rng, P, [S] * n, "spread")]
+    res = score_shared_batch(scorer, batches)
+    p_ref = oracle_scores(ow, batches)
+    dp = np.abs(res.p_yes - p_ref)
+    print(f"{name}: max|dp|={dp.max():.2e}")
+    assert dp.max() <= TOL_P
