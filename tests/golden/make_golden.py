@@ -1,0 +1,72 @@
+"""Generate tests/golden/prompts.json from the REFERENCE package (run in the build container only;
+/root/reference does not exist on the GPU box — the committed JSON travels instead).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Imports the reference's own tokenizer.py and corpus.py (the only executable parts of the path,
+SURVEY.md §0) and records:
+  * the Vocab special-id table and FNV-1a constants (tokenizer.py:22-37, :49-76);
+  * encode() known answers (SYSTEM_PREFIX, "<|ans|>", "yes", "no", "rust engineer", "");
+  * Eq-1 prompts (corpus.assemble_prompt, corpus.py:302-311) for seeded queries x items, truncated
+    to the 2048-token budget (corpus.truncate_description, corpus.py:314-345), as token ids, plus the
+    per-segment token counts — the golden inputs for split_shared_prefix / packing parity;
+  * a truncation known answer (budget 300) and the PromptBudgetError message for a tiny budget.
+"""
+
+import json
+import os
+import sys
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+from prefrank import corpus, tokenizer  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "prompts.json")
+
+
+def main():
+    vocab = tokenizer.Vocab()
+    enc = lambda s: tokenizer.encode(s, vocab)
+    queries, items = corpus.generate_corpus(7, 4, 40)
+    requests = []
+    for qi, q in enumerate(queries):
+        cands = items[qi * 8: qi * 8 + 8]
+        prompts, seg_lens = [], []
+        for it in cands:
+            seg = corpus.truncate_description(corpus.assemble_prompt(q, it), 2048, vocab)
+            full = enc(seg.full_prompt())
+            parts = [enc(seg.system_prefix), enc(seg.query_text), enc(seg.metadata_text),
+                     enc(seg.description_text), enc(seg.suffix)]
+            assert sum(parts, []) == full
+            prompts.append(full)
+            seg_lens.append([len(p) for p in parts])
+        requests.append({"query_id": q.id, "item_ids": [it.id for it in cands],
+                         "prompts": prompts, "segment_lens": seg_lens})
+    seg = corpus.assemble_prompt(queries[0], items[0])
+    trunc300 = enc(corpus.truncate_description(seg, 300, vocab).full_prompt())
+    try:
+        corpus.truncate_description(seg, 10, vocab)
+        budget_err = None
+    except corpus.PromptBudgetError as e:
+        budget_err = str(e)
+    golden = {
+        "generator": "tests/golden/make_golden.py (reference prefrank tokenizer.py + corpus.py)",
+        "fnv": {"offset": tokenizer.FNV_OFFSET, "prime": tokenizer.FNV_PRIME,
+                "fnv1a_64": {w: tokenizer.fnv1a_64(w.encode()) for w in ["rust", "engineer", "a", ""]}},
+        "vocab": vocab.to_config(),
+        "encode": {s: enc(s) for s in [corpus.SYSTEM_PREFIX, "<|ans|>", "yes", "no", "rust engineer", "",
+                                       "Senior Rust Engineer, Berlin!"]},
+        "word_id": {w: vocab.word_id(w) for w in ["rust", "python", "yes", "<|meta|>"]},
+        "requests": requests,
+        "truncate_300": {"len": len(trunc300), "ends_with": trunc300[-3:]},
+        "budget_error": budget_err,
+    }
+    with open(OUT, "w") as f:
+        json.dump(golden, f, separators=(",", ":"))
+    print(f"wrote {OUT}: {len(requests)} requests, {sum(len(r['prompts']) for r in requests)} prompts")
+
+
+if __name__ == "__main__":
+    main()
