@@ -5,255 +5,314 @@
 //     dense  : rows [kv_off, kv_off + kv_len)        (the shared query prefix; may be empty)
 //     causal : rows [q_off, q_off + 1 + local index) (the segment's own tokens)
 // The prefix segment itself is {kv_len = 0, q = prefix rows}.  The prefix K/V are computed once
-// per request by the QKV GEMM and read by every item's CTA; nothing is retained afterwards.
-// Online softmax over the concatenated key blocks is algebraically the LSE merge of the
+// per request by the QKV GEMM and read by every item's work unit; nothing is retained after the
+// call.  Online softmax over the concatenated key blocks is algebraically the LSE merge of the
 // prefix and suffix partials.
 //
-// One CTA = (128-row query tile of one segment, one query head).  Warp roles:
-//   warps 0..3  softmax: thread i owns query row i (TMEM lane i) — tcgen05.ld S, mask, online
-//               max/sum, P -> bf16 swizzled smem, O accumulated in registers from TMEM O_blk
-//   warp 4      TMA producer: Q once, K/V 128-key blocks double-buffered
-//   warp 5      tcgen05.mma issuer: S = Q.K^T (M128 N128 K128), O_blk = P.V (V MN-major)
+// Persistent kernel, one CTA per SM.  Work unit = (128-row query tile, GQA kv-head g, pair of
+// query heads sharing g): both heads reuse every K/V block loaded.  64-key blocks (a 64-token
+// prefix is one block; a 100-token item two).  Warp roles (384 threads):
+//   WG0 / WG1   softmax for query head 0 / 1 of the pair: thread i owns row i (TMEM lane i);
+//               tcgen05.ld S -> mask -> exp2 -> bf16 P (swizzled smem).  O is accumulated by
+//               the tensor core in TMEM; the running max is only raised (and O rescaled in
+//               TMEM) when it grows by > 2^8 (lazy rescale), so most blocks never touch O.
+//   warp 8      TMA producer: Q pair per unit; K/V 64-key blocks through a 3-stage ring
+//   warp 9      TMEM owner + tcgen05.mma issuer: S_j = Q_j K^T (M128 N64 K128),
+//               O_j += P_j V (M128 N128 K64, V MN-major), ping-ponging the two heads
 #include <cuda_runtime.h>
 #include "ptx.cuh"
 #include "pf_internal.h"
 
 namespace pf {
 
-constexpr int ATT_THREADS = 192;
-constexpr int ATT_TILE = 16384;                 // 128 rows x 64 bf16 (one SW128 box)
-constexpr int ATT_OPER = 2 * ATT_TILE;          // 128 x 128 bf16 operand = 32 KB
-constexpr int ATT_SMEM = 1024 + 6 * ATT_OPER + 256;   // Q, K[2], V[2], P
+constexpr int AT_THREADS = 384;
+constexpr int AT_KB = 64;                       // keys per block
+constexpr int AT_STAGES = 3;
+constexpr int AT_QBOX = 128 * 64 * 2;           // [128 rows x 64 cols] bf16 = 16 KB
+constexpr int AT_KBOX = 64 * 64 * 2;            // [64 rows x 64 cols] bf16 = 8 KB
+constexpr int AT_Q_HEAD = 2 * AT_QBOX;          // one head's Q tile (dh = 128)
+constexpr int AT_KV_STAGE = 4 * AT_KBOX;        // K (2 boxes) + V (2 boxes)
+constexpr int AT_P_HEAD = 128 * 128;            // [128 rows x 64 keys] bf16
+constexpr int AT_OFF_KV = 2 * AT_Q_HEAD;
+constexpr int AT_OFF_P = AT_OFF_KV + AT_STAGES * AT_KV_STAGE;
+constexpr int AT_OFF_BAR = AT_OFF_P + 2 * AT_P_HEAD;
+constexpr int AT_SMEM = 1024 + AT_OFF_BAR + 256;
+constexpr float AT_RESCALE_THRESH = 8.0f;       // log2 units
 
-__global__ void __launch_bounds__(ATT_THREADS, 1)
-    attn_prefix_kernel(const __grid_constant__ CUtensorMap tmQKV, const AttnDesc d) {
+struct UnitInfo {
+  int q_row0, q_len, q_local0, kv_off, kv_len, q_off, n_pre, n_blk, h0, nh, g;
+};
+
+PF_DEVICE UnitInfo decode_unit(const AttnDesc& d, int u, int r, int n_pairs) {
+  UnitInfo ui;
+  const int per_w = d.Hkv * n_pairs;
+  const int w = u / per_w;
+  const int rem = u - w * per_w;
+  ui.g = rem / n_pairs;
+  const int p = rem - ui.g * n_pairs;
+  const int4 wk = reinterpret_cast<const int4*>(d.work)[w];
+  const int4 sg = reinterpret_cast<const int4*>(d.segs)[wk.x];
+  const int qt = wk.y;
+  ui.kv_off = sg.x; ui.kv_len = sg.y; ui.q_off = sg.z; ui.q_len = sg.w;
+  ui.q_local0 = qt * 128;
+  ui.q_row0 = sg.z + qt * 128;
+  ui.n_pre = (sg.y + AT_KB - 1) / AT_KB;
+  const int q_end = min(qt * 128 + 128, sg.w);
+  ui.n_blk = ui.n_pre + (q_end + AT_KB - 1) / AT_KB;
+  ui.h0 = ui.g * r + 2 * p;
+  ui.nh = min(2, r - 2 * p);
+  return ui;
+}
+
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attn_prefix_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                       const AttnDesc d, int n_units) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + ATT_OPER;           // 2 stages
-  uint8_t* sV = smem + 3 * ATT_OPER;       // 2 stages
-  uint8_t* sP = smem + 5 * ATT_OPER;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * ATT_OPER);
+  uint8_t* sKV = smem + AT_OFF_KV;
+  uint8_t* sP = smem + AT_OFF_P;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AT_OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_ready = bars + 6;
-  uint64_t* o_full = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;            // [3]
+  uint64_t* kv_empty = bars + 5;           // [3]
+  uint64_t* s_full = bars + 8;             // [2]
+  uint64_t* p_ready = bars + 10;           // [2]
+  uint64_t* o_done = bars + 12;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-
-  const int4 wk = reinterpret_cast<const int4*>(d.work)[blockIdx.x];
-  const int seg = wk.x, qt = wk.y;
-  const int4 sg = reinterpret_cast<const int4*>(d.segs)[seg];
-  const int kv_off = sg.x, kv_len = sg.y, q_off = sg.z, q_len = sg.w;
-  const int h = blockIdx.y;
-  const int g = h / (d.H / d.Hkv);
-  const int q_row0 = q_off + qt * 128;
-  const int n_pre = (kv_len + 127) / 128;
-  const int n_blk = n_pre + qt + 1;
-  const int q_col = h * d.dh;
-  const int k_col = (d.H + g) * d.dh;
-  const int v_col = (d.H + d.Hkv + g) * d.dh;
+  const int r = d.H / d.Hkv;
+  const int n_pairs = (r + 1) / 2;
 
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmKV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    mbar_init(s_full, 1);
-    mbar_init(p_ready, 4);
-    mbar_init(o_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < AT_STAGES; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int j = 0; j < 2; ++j) { mbar_init(&s_full[j], 1); mbar_init(&p_ready[j], 4); mbar_init(&o_done[j], 1); }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<256>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tS = tmem_base;         // cols [0,128)
-  const uint32_t tO = tmem_base + 128;   // cols [128,256)
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, ATT_OPER);
-      tma_load_2d(sQ, &tmQKV, q_full, q_col, q_row0, kEvictFirst);
-      tma_load_2d(sQ + ATT_TILE, &tmQKV, q_full, q_col + 64, q_row0, kEvictFirst);
-      for (int b = 0; b < n_blk; ++b) {
-        const int s = b & 1;
-        mbar_wait(&kv_empty[s], ((b >> 1) & 1) ^ 1);
-        const int krow = (b < n_pre) ? (kv_off + b * 128) : (q_off + (b - n_pre) * 128);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * ATT_OPER);
-        uint8_t* k_dst = sK + s * ATT_OPER;
-        uint8_t* v_dst = sV + s * ATT_OPER;
-        tma_load_2d(k_dst, &tmQKV, &kv_full[s], k_col, krow, kEvictLast);
-        tma_load_2d(k_dst + ATT_TILE, &tmQKV, &kv_full[s], k_col + 64, krow, kEvictLast);
-        tma_load_2d(v_dst, &tmQKV, &kv_full[s], v_col, krow, kEvictLast);
-        tma_load_2d(v_dst + ATT_TILE, &tmQKV, &kv_full[s], v_col + 64, krow, kEvictLast);
+      // ------------------------------------------------------------------ TMA producer
+      uint32_t kv_it = 0, q_it = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const UnitInfo ui = decode_unit(d, u, r, n_pairs);
+        mbar_wait(q_empty, (q_it & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, ui.nh * AT_Q_HEAD);
+        for (int j = 0; j < ui.nh; ++j) {
+          const int qc = (ui.h0 + j) * d.dh;
+          tma_load_2d(sQ + j * AT_Q_HEAD, &tmQ, q_full, qc, ui.q_row0, kEvictFirst);
+          tma_load_2d(sQ + j * AT_Q_HEAD + AT_QBOX, &tmQ, q_full, qc + 64, ui.q_row0, kEvictFirst);
+        }
+        ++q_it;
+        const int kc = (d.H + ui.g) * d.dh;
+        const int vc = (d.H + d.Hkv + ui.g) * d.dh;
+        for (int b = 0; b < ui.n_blk; ++b, ++kv_it) {
+          const int st = kv_it % AT_STAGES;
+          mbar_wait(&kv_empty[st], ((kv_it / AT_STAGES) & 1) ^ 1);
+          const int krow = b < ui.n_pre ? ui.kv_off + b * AT_KB : ui.q_off + (b - ui.n_pre) * AT_KB;
+          uint8_t* dst = sKV + st * AT_KV_STAGE;
+          mbar_arrive_expect_tx(&kv_full[st], AT_KV_STAGE);
+          tma_load_2d(dst, &tmKV, &kv_full[st], kc, krow, kEvictLast);
+          tma_load_2d(dst + AT_KBOX, &tmKV, &kv_full[st], kc + 64, krow, kEvictLast);
+          tma_load_2d(dst + 2 * AT_KBOX, &tmKV, &kv_full[st], vc, krow, kEvictLast);
+          tma_load_2d(dst + 3 * AT_KBOX, &tmKV, &kv_full[st], vc + 64, krow, kEvictLast);
+        }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      // ------------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, AT_KB, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);   // V is MN-major
-      mbar_wait(q_full, 0);
+      uint32_t kv_it = 0, q_it = 0;
+      uint32_t blk_it[2] = {0, 0};
       const uint32_t q_addr = smem_u32(sQ);
       const uint32_t p_addr = smem_u32(sP);
-      for (int b = 0; b < n_blk; ++b) {
-        const int s = b & 1;
-        mbar_wait(&kv_full[s], (b >> 1) & 1);
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const UnitInfo ui = decode_unit(d, u, r, n_pairs);
+        mbar_wait(q_full, q_it & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + s * ATT_OPER);
-        const uint32_t v_addr = smem_u32(sV + s * ATT_OPER);
-        // S = Q . K^T over dh = 128 (8 x K16 steps; 64-col boxes at +16 KB)
+        for (int b = 0; b < ui.n_blk; ++b, ++kv_it) {
+          const int st = kv_it % AT_STAGES;
+          mbar_wait(&kv_full[st], (kv_it / AT_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(sKV + st * AT_KV_STAGE);
+          const uint32_t v_addr = k_addr + 2 * AT_KBOX;
+          for (int j = 0; j < ui.nh; ++j) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t off = (k >> 2) * ATT_TILE + (k & 3) * 32;
-          umma_bf16_ss(tS, kmajor_desc(q_addr + off), kmajor_desc(k_addr + off), idesc_s, k != 0);
-        }
-        umma_commit(s_full);
-        mbar_wait(p_ready, b & 1);
-        tc_fence_after();
-        // O_blk = P . V over 128 keys: P K-major (keys contiguous), V MN-major (dh contiguous;
-        // the two 64-wide dh boxes sit 16 KB apart = LBO, 8-key groups 1 KB apart = SBO).
+            for (int k = 0; k < 8; ++k) {
+              umma_bf16_ss(tmem_base + j * AT_KB,
+                           kmajor_desc(q_addr + j * AT_Q_HEAD + (k >> 2) * AT_QBOX + (k & 3) * 32),
+                           kmajor_desc(k_addr + (k >> 2) * AT_KBOX + (k & 3) * 32), idesc_s, k != 0);
+            }
+            umma_commit(&s_full[j]);
+          }
+          if (b == ui.n_blk - 1) umma_commit(q_empty);
+          for (int j = 0; j < ui.nh; ++j) {
+            mbar_wait(&p_ready[j], blk_it[j] & 1);
+            ++blk_it[j];
+            tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t poff = (k >> 2) * ATT_TILE + (k & 3) * 32;
-          umma_bf16_ss(tO, kmajor_desc(p_addr + poff), sw128_desc(v_addr + k * 2048, ATT_TILE, 1024),
-                       idesc_o, k != 0);
+            for (int k = 0; k < AT_KB / 16; ++k) {
+              umma_bf16_ss(tmem_base + 128 + j * 128, kmajor_desc(p_addr + j * AT_P_HEAD + k * 32),
+                           sw128_desc(v_addr + k * 2048, AT_KBOX, 1024), idesc_o, (b | k) != 0);
+            }
+            if (b == ui.n_blk - 1) umma_commit(&o_done[j]);
+          }
+          umma_commit(&kv_empty[st]);
         }
-        umma_commit(o_full);
-        umma_commit(&kv_empty[s]);
+        ++q_it;
       }
     }
-  } else {
-    // ---------------------------------------------------------------- softmax warps 0..3
-    const uint32_t row = warp * 32 + lane;
-    const int q_local = qt * 128 + (int)row;            // index within the segment
-    const float sl2 = d.scale * 1.4426950408889634f;   // scale * log2(e)
-    const uint32_t lane_base = (warp * 32) << 16;
-    float o_acc[128];
+  } else if (warp < 8) {
+    // -------------------------------------------------------------------- softmax WG j
+    const int j = warp >> 2;
+    const uint32_t row = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = ((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem_base + lane_base + j * AT_KB;
+    const uint32_t tO = tmem_base + lane_base + 128 + j * 128;
+    const uint32_t p_row = smem_u32(sP + j * AT_P_HEAD) + row * 128;
+    const float sl2 = d.scale * 1.4426950408889634f;
+    uint32_t blk_it = 0, u_it = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const UnitInfo ui = decode_unit(d, u, r, n_pairs);
+      if (j >= ui.nh) continue;
+      const int q_local = ui.q_local0 + (int)row;
+      float m_used = -INFINITY, l_run = 0.f;
+      for (int b = 0; b < ui.n_blk; ++b, ++blk_it) {
+        const bool is_pre = b < ui.n_pre;
+        const int lim = is_pre ? (ui.kv_len - b * AT_KB) : (q_local - (b - ui.n_pre) * AT_KB + 1);
+        mbar_wait(&s_full[j], blk_it & 1);
+        tc_fence_after();
+        uint32_t s[2][32];
+        tmem_ld_32x32b_x32(tS, s[0]);
+        tmem_ld_32x32b_x32(tS + 32, s[1]);
+        tmem_ld_wait();
+        float mx = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 128; ++j) o_acc[j] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f, alpha_prev = 1.f;
-    const uint32_t p_base = smem_u32(sP);
-
-    for (int b = 0; b < n_blk; ++b) {
-      const bool is_pre = b < n_pre;
-      // valid keys in this block: dense part -> j < kv_len - b*128 ; causal -> j <= q_local - kb0
-      const int lim = is_pre ? (kv_len - b * 128) : (q_local - (b - n_pre) * 128 + 1);
-      mbar_wait(s_full, b & 1);
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = (c * 32 + i < lim) ? __uint_as_float(s[c][i]) * sl2 : -INFINITY;
+            s[c][i] = __float_as_uint(x);
+            mx = fmaxf(mx, x);
+          }
+        const bool need = mx > m_used + AT_RESCALE_THRESH;
+        bool rescaled = false;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = fmaxf(m_used, mx);
+          if (b > 0) {
+            const float alpha = exp2f(m_used - m_new);
+            l_run *= alpha;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld_32x32b_x32(tO + c * 32, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st_32x32b_x32(tO + c * 32, o);
+            }
+            rescaled = true;
+          }
+          m_used = m_new;
+        }
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = exp2f(__uint_as_float(s[c][2 * i]) - m_used);
+            const float p1 = exp2f(__uint_as_float(s[c][2 * i + 1]) - m_used);
+            sum += p0 + p1;
+            w[i] = pack_bf16x2(p0, p1);
+          }
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint32_t chunk = c * 4 + q4;
+            st_shared_v4(p_row + ((chunk ^ (row & 7)) << 4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2],
+                         w[4 * q4 + 3]);
+          }
+        }
+        l_run += sum;
+        if (rescaled) tmem_st_wait();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_ready[j]);
+      }
+      // ---- unit epilogue: O / l -> bf16 -> global
+      mbar_wait(&o_done[j], u_it & 1);
+      ++u_it;
       tc_fence_after();
-      // pass 1: row max
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + lane_base + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float x = (c * 32 + j < lim) ? __uint_as_float(v[j]) * sl2 : -INFINITY;
-          mx = fmaxf(mx, x);
-        }
-      }
-      const float m_new = fmaxf(m_run, mx);
-      const float alpha = exp2f(m_run - m_new);   // m_run = -inf on the first block -> 0
-      // pass 2: P = exp2(s - m_new) -> bf16 smem (SW128, K-major over keys), row sum
-      float sum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + lane_base + c * 32, v);
-        tmem_ld_wait();
-        uint32_t w[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int j0 = c * 32 + 2 * j;
-          const float p0 = (j0 < lim) ? exp2f(__uint_as_float(v[2 * j]) * sl2 - m_new) : 0.f;
-          const float p1 = (j0 + 1 < lim) ? exp2f(__uint_as_float(v[2 * j + 1]) * sl2 - m_new) : 0.f;
-          sum += p0 + p1;
-          w[j] = pack_bf16x2(p0, p1);
-        }
-        // 32 keys = 64 B = four 16 B chunks; box (c >> 1), chunk index within the 128 B row
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t chunk = (c & 1) * 4 + q4;
-          const uint32_t addr = p_base + (c >> 1) * ATT_TILE + row * 128 + ((chunk ^ (row & 7)) << 4);
-          st_shared_v4(addr, w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
-        }
-      }
-      // fold in the previous block's P.V before the next PV MMA overwrites it
-      if (b > 0) {
-        mbar_wait(o_full, (b - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tO + lane_base + c * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o_acc[c * 32 + j] = o_acc[c * 32 + j] * alpha_prev + __uint_as_float(v[j]);
-        }
-      }
-      l_run = l_run * alpha + sum;
-      m_run = m_new;
-      alpha_prev = alpha;
-      fence_proxy_async_smem();   // P visible to the tensor core (async proxy)
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
-    }
-    mbar_wait(o_full, (n_blk - 1) & 1);
-    tc_fence_after();
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(tO + lane_base + c * 32, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) o_acc[c * 32 + j] = o_acc[c * 32 + j] * alpha_prev + __uint_as_float(v[j]);
-    }
-    if (q_local < q_len) {
       const float inv = 1.f / l_run;
+      const bool valid = q_local < ui.q_len;
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(d.out) +
-                                            (size_t)(q_row0 + row) * (d.H * d.dh) + h * d.dh);
+                                            (size_t)(ui.q_row0 + row) * (d.H * d.dh) + (ui.h0 + j) * d.dh);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tO + c * 32, o);
+        tmem_ld_wait();
+        if (valid) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        uint4 u;
-        u.x = pack_bf16x2(o_acc[8 * j + 0] * inv, o_acc[8 * j + 1] * inv);
-        u.y = pack_bf16x2(o_acc[8 * j + 2] * inv, o_acc[8 * j + 3] * inv);
-        u.z = pack_bf16x2(o_acc[8 * j + 4] * inv, o_acc[8 * j + 5] * inv);
-        u.w = pack_bf16x2(o_acc[8 * j + 6] * inv, o_acc[8 * j + 7] * inv);
-        dst[j] = u;
+          for (int q = 0; q < 4; ++q) {
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            v.y = pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            v.z = pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            v.w = pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            dst[c * 4 + q] = v;
+          }
+        }
       }
+      tc_fence_before();
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem_base);
+    tmem_dealloc<512>(tmem_base);
   }
 }
+
+static int g_att_sms = 0;
 
 int launch_attention(const AttnDesc& d, cudaStream_t stream) {
   if (d.dh != 128) return fail(-2, "attention: d_head must be 128 (got %d)", d.dh);
   if (d.H % d.Hkv != 0) return fail(-2, "attention: n_heads %% n_kv_heads != 0");
   if (d.n_work == 0) return 0;
   const int ldq = (d.H + 2 * d.Hkv) * d.dh;
-  CUtensorMap tm;
-  if (!make_tmap_2d(&tm, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, 128, 64, true))
-    return -3;
+  CUtensorMap tq, tkv;
+  if (!make_tmap_2d(&tq, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, 128, 64, true)) return -3;
+  if (!make_tmap_2d(&tkv, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, AT_KB, 64, true)) return -3;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM);
+    cudaFuncSetAttribute(attn_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_att_sms, cudaDevAttrMultiProcessorCount, dev);
     attr_set = true;
   }
-  dim3 grid(d.n_work, d.H);
-  attn_prefix_kernel<<<grid, ATT_THREADS, ATT_SMEM, stream>>>(tm, d);
+  const int r = d.H / d.Hkv;
+  const int n_units = d.n_work * d.Hkv * ((r + 1) / 2);
+  const int grid = n_units < g_att_sms ? n_units : g_att_sms;
+  attn_prefix_kernel<<<grid, AT_THREADS, AT_SMEM, stream>>>(tq, tkv, d, n_units);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(-4, "attention launch: %s", cudaGetErrorString(e));
   return 0;

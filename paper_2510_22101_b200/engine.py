@@ -128,7 +128,8 @@ class PrefillScorer:
         return ctypes.c_void_p(s.cuda_stream)
 
     # ------------------------------------------------------------------ scoring
-    def score_device(self, dp: DevicePacked, logits2=None, p_yes=None, stream=None, check=True):
+    def score_device(self, dp: DevicePacked, logits2=None, p_yes=None, stream=None, check=True,
+                     workspace=None):
         """Inputs already resident on the device; asynchronous.  Returns device tensors."""
         import torch
 
@@ -138,7 +139,7 @@ class PrefillScorer:
             logits2 = torch.empty((n, 2), dtype=torch.float32, device=self.device)
         if p_yes is None:
             p_yes = torch.empty((n,), dtype=torch.float32, device=self.device)
-        ws, ws_bytes = self.workspace(pk.T, n)
+        ws, ws_bytes = workspace if workspace is not None else self.workspace(pk.T, n)
         if check:
             self._bad.zero_()
         rc = self.lib.pf_score(self.handle, _ptr(dp.ids), _ptr(dp.pos), _ptr(dp.segs), len(pk.segs),
@@ -147,6 +148,33 @@ class PrefillScorer:
                                self._stream(stream))
         _lib.check(rc)
         return logits2, p_yes
+
+    def graph_runner(self, dp: DevicePacked):
+        """Capture one pf_score pass over ``dp`` into a CUDA graph (private workspace and output
+        buffers, so later calls cannot invalidate it).  Returns ``run() -> (logits2, p_yes)``;
+        replay removes the ~200 host launches per pass."""
+        import torch
+
+        pk = dp.packed
+        n = pk.n_items
+        need = int(self.lib.pf_workspace_bytes(self.handle, pk.T, n))
+        ws_t = torch.empty(need + 4096, dtype=torch.uint8, device=self.device)
+        base = _ptr(ws_t)
+        ws = ((base + 1023) & ~1023, ws_t.numel() - (((base + 1023) & ~1023) - base))
+        logits2 = torch.empty((n, 2), dtype=torch.float32, device=self.device)
+        p_yes = torch.empty((n,), dtype=torch.float32, device=self.device)
+        self.score_device(dp, logits2, p_yes, workspace=ws)   # first launch sets kernel attributes
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.score_device(dp, logits2, p_yes, workspace=ws)
+
+        def run():
+            g.replay()
+            return logits2, p_yes
+
+        run.graph, run.keepalive = g, (ws_t, dp)
+        return run
 
     def score_host(self, pp: PinnedPacked, stream=None) -> ScoredBatch:
         """End-to-end through the C-ABI with host buffers (H2D + forward + D2H + sync)."""

@@ -118,6 +118,41 @@ def test_host_path_matches_device_path():
     np.testing.assert_array_equal(dev.logits2, host.logits2)
 
 
+def test_pruned_model_parity():
+    """Pruned widths (d_ff 600 -> 360, padded to 384 on the device; one GQA group dropped) score
+    within tolerance of the oracle on the same compacted weights."""
+    from paper_2510_22101_b200.pruning import PruneRecipe, apply_recipe
+
+    cfg = CONFIGS["TINY_GQA"]
+    pw = apply_recipe(init_weights(cfg, 0), PruneRecipe(mlp_sparsity=0.4, kv_groups_to_keep=1))
+    assert pw.config.d_ff == 360 and pw.config.n_heads == 2
+    scorer = PrefillScorer(pw)
+    ow = OM.OracleWeights(pw.config, pw.token_embedding,
+                          [{**{f: getattr(lw, f) for f in OM.LAYER_FIELDS},
+                            "rms_attn": lw.rms_attn, "rms_mlp": lw.rms_mlp} for lw in pw.layers],
+                          pw.final_norm, pw.head)
+    rng = np.random.default_rng(21)
+    batches = [make_shared(rng, 40, list(rng.integers(1, 200, 16)), "spread")]
+    res = score_shared_batch(scorer, batches)
+    p_ref = oracle_scores(ow, batches)
+    assert np.max(np.abs(res.p_yes - p_ref)) <= TOL_P
+
+
+def test_graph_replay_matches_direct():
+    from paper_2510_22101_b200.engine import DevicePacked
+
+    cfg, scorer, _ = get_models("TINY_GQA")
+    rng = np.random.default_rng(9)
+    packed = pack_requests([make_shared(rng, 64, list(rng.integers(1, 300, 20)), "spread")])
+    direct = scorer.score_packed(packed)
+    run = scorer.graph_runner(DevicePacked(packed, scorer.device))
+    for _ in range(3):
+        logits2, p_yes = run()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(p_yes.cpu().numpy(), direct.p_yes)
+    np.testing.assert_array_equal(logits2.cpu().numpy(), direct.logits2)
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("name,P,S,n", [("C4", 64, 100, 8), ("C2", 64, 128, 6)])
 def test_model_parity_full_size(name, P, S, n):

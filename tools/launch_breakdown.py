@@ -1,0 +1,36 @@
+"""Per-kernel share of one step from an ncu launch list (gpu__time_duration.sum CSV).
+    python tools/launch_breakdown.py gpurun_out/launches_c4.csv"""
+import collections
+import csv
+import re
+import sys
+
+EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add(O/down)"}
+
+
+def main(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h, data = rows[hi], rows[hi + 1:]
+    ki, mi, vi, ui = (h.index(c) for c in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in data:
+        if r[mi] != "gpu__time_duration.sum":
+            continue
+        name = r[ki]
+        m = re.search(r"gemm_bf16_kernel<(\d)>", name)
+        key = f"gemm<{EPI.get(m.group(1), m.group(1))}>" if m else re.sub(r"^void |pf::|\(.*", "", name).split("<")[0]
+        v = float(r[vi].replace(",", ""))
+        if r[ui] == "usecond":
+            v *= 1e3
+        agg[key][0] += 1
+        agg[key][1] += v
+    tot = sum(v[1] for v in agg.values())
+    print(f"{'kernel':28s} {'share':>7s} {'n':>5s} {'avg us':>9s} {'total us':>10s}")
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{k:28s} {t / tot * 100:6.2f}% {n:5d} {t / n / 1e3:9.1f} {t / 1e3:10.1f}")
+    print(f"{'TOTAL':28s} {'':7s} {sum(v[0] for v in agg.values()):5d} {'':9s} {tot / 1e3:10.1f}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
