@@ -159,10 +159,10 @@ int pf_model_create(const pf_model_desc* desc, pf_model** out) {
   m->tm_gu.resize(L);
   m->tm_down.resize(L);
   for (int l = 0; l < L; ++l) {
-    bool ok = make_tmap_2d(&m->tm_qkv[l], m->w_qkv[l], 2, m->qkv_n, d.d_model, d.d_model, 256, 64, true) &&
-              make_tmap_2d(&m->tm_o[l], m->w_o[l], 2, d.d_model, m->attn_k, m->attn_k, 256, 64, true) &&
-              make_tmap_2d(&m->tm_gu[l], m->w_gu[l], 2, 2 * d.d_ff_pad, d.d_model, d.d_model, 256, 64, true) &&
-              make_tmap_2d(&m->tm_down[l], m->w_down[l], 2, d.d_model, d.d_ff_pad, d.d_ff_pad, 256, 64, true);
+    bool ok = make_weight_tmap(&m->tm_qkv[l], m->w_qkv[l], m->qkv_n, d.d_model, d.d_model) &&
+              make_weight_tmap(&m->tm_o[l], m->w_o[l], d.d_model, m->attn_k, m->attn_k) &&
+              make_weight_tmap(&m->tm_gu[l], m->w_gu[l], 2 * d.d_ff_pad, d.d_model, d.d_model) &&
+              make_weight_tmap(&m->tm_down[l], m->w_down[l], d.d_model, d.d_ff_pad, d.d_ff_pad);
     if (!ok) { delete m; return -3; }
   }
   *out = m;

@@ -14,23 +14,32 @@
 //   EPI_SWIGLU     gate/up projection with B rows interleaved per 128-neuron block
 //                  ([gate_j | up_j] per 256-row tile); writes silu(gate)*up as bf16 (N/2 cols)
 //   EPI_RESID_ADD  O / down projection: fp32 residual stream += acc via TMA reduce-add
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "ptx.cuh"
 #include "pf_internal.h"
 
 namespace pf {
 
-constexpr int GEMM_BM = 128;
-constexpr int GEMM_BN = 256;
+constexpr int GEMM_BM = 128;                          // rows per CTA (TMEM lanes)
+constexpr int GEMM_BN = 256;                          // output columns per tile (both CG modes)
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_STAGES = 4;
 constexpr int GEMM_THREADS = 192;
 constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
-constexpr int GEMM_B_BYTES = GEMM_BN * GEMM_BK * 2;   // 32 KB
-constexpr int GEMM_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES;
 constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B staging box
-constexpr int GEMM_SMEM_BYTES =
-    1024 + GEMM_STAGES * GEMM_STAGE_BYTES + 4 * 2 * GEMM_STG_BYTES + 256;
+
+// CG = CTAs per MMA (cta_group).  CG=2: a CTA pair computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M=256); each CTA loads its own 128 A rows and half (128) of the
+// B rows, so per-CTA operand bytes per MMA drop from 48 KB to 32 KB per k-block.
+template <int CG>
+struct GemmCfg {
+  static constexpr int B_ROWS = GEMM_BN / CG;                // B rows loaded per CTA
+  static constexpr int B_BYTES = B_ROWS * GEMM_BK * 2;
+  static constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 4 * 2 * GEMM_STG_BYTES + 256;
+  static constexpr int TILE_M = GEMM_BM * CG;
+};
 
 struct GemmArgs {
   int M, N, K;
@@ -52,74 +61,90 @@ PF_DEVICE void stage_row_128B(uint32_t stg, uint32_t row, const uint32_t (&w)[32
   }
 }
 
-template <int EPI>
+template <int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
+  using Cfg = GemmCfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + GEMM_STAGES * GEMM_A_BYTES;
-  uint8_t* sStg = smem + GEMM_STAGES * GEMM_STAGE_BYTES;
+  uint8_t* sB = smem + Cfg::STAGES * GEMM_A_BYTES;
+  uint8_t* sStg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 2 * GEMM_STG_BYTES);
   uint64_t* full_bar = bars;
-  uint64_t* empty_bar = bars + GEMM_STAGES;
-  uint64_t* tfull_bar = bars + 2 * GEMM_STAGES;
-  uint64_t* tempty_bar = bars + 2 * GEMM_STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * GEMM_STAGES + 4);
+  uint64_t* empty_bar = bars + Cfg::STAGES;
+  uint64_t* tfull_bar = bars + 2 * Cfg::STAGES;
+  uint64_t* tempty_bar = bars + 2 * Cfg::STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int num_tiles = args.num_m_blk * args.num_n_blk;
+  const int num_tiles = args.num_m_blk * args.num_n_blk;   // num_m_blk counts TILE_M rows
   const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
+  // persistent schedule over CTA groups (a pair shares one tile)
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const int grp = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int ngrp = CG == 2 ? (int)nclusters_x() : (int)gridDim.x;
+  const bool leader = rank == 0;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
-    for (int s = 0; s < GEMM_STAGES; ++s) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], 4 * CG);   // every epilogue warp of the group arrives
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer
+      // ------------------------------------------------------------ TMA producer (each CTA)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / args.num_n_blk) * GEMM_BM;
-        const int n0 = (tile % args.num_n_blk) * GEMM_BN;
+      for (int tile = grp; tile < num_tiles; tile += ngrp) {
+        const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
+        const int n0 = (tile % args.num_n_blk) * GEMM_BN + rank * Cfg::B_ROWS;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], GEMM_STAGE_BYTES);
-          tma_load_2d(sA + stage * GEMM_A_BYTES, &tmA, &full_bar[stage], kb * GEMM_BK, m0);
-          tma_load_2d(sB + stage * GEMM_B_BYTES, &tmB, &full_bar[stage], kb * GEMM_BK, n0,
-                      kEvictLast);
-          if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+          if constexpr (CG == 2) {
+            // both CTAs' bytes complete on the leader's barrier; only the leader arms it
+            const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], CG * Cfg::STAGE_BYTES);
+            tma_load_2d_pair(sA + stage * GEMM_A_BYTES, &tmA, lbar, kb * GEMM_BK, m0, kEvictNormal);
+            tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, lbar, kb * GEMM_BK, n0, kEvictLast);
+          } else {
+            mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+            tma_load_2d(sA + stage * GEMM_A_BYTES, &tmA, &full_bar[stage], kb * GEMM_BK, m0);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full_bar[stage], kb * GEMM_BK, n0, kEvictLast);
+          }
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, GEMM_BN, false, false);
+    if (lane == 0 && leader) {
+      // ------------------------------------------------------------ MMA issuer (leader CTA)
+      constexpr uint32_t idesc = make_idesc_bf16(Cfg::TILE_M, GEMM_BN, false, false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = grp; tile < num_tiles; tile += ngrp) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * GEMM_BN;
@@ -127,16 +152,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * GEMM_A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * GEMM_B_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k) {
-            umma_bf16_ss(d_tmem, kmajor_desc(a_addr + k * 32), kmajor_desc(b_addr + k * 32), idesc,
-                         (kb | k) != 0 ? 1u : 0u);
+            if constexpr (CG == 2)
+              umma_bf16_ss_pair(d_tmem, kmajor_desc(a_addr + k * 32), kmajor_desc(b_addr + k * 32), idesc,
+                                (kb | k) != 0 ? 1u : 0u);
+            else
+              umma_bf16_ss(d_tmem, kmajor_desc(a_addr + k * 32), kmajor_desc(b_addr + k * 32), idesc,
+                           (kb | k) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
-          if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+          if constexpr (CG == 2) umma_commit_pair(&empty_bar[stage], 0x3);
+          else umma_commit(&empty_bar[stage]);
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (CG == 2) umma_commit_pair(&tfull_bar[acc], 0x3);
+        else umma_commit(&tfull_bar[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -166,8 +197,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       stg_idx ^= 1;
     };
 
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile / args.num_n_blk) * GEMM_BM;
+    // the MMA issuer waits on the leader's tmem-empty barrier
+    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0),
+                                       mapa_shared(smem_u32(&tempty_bar[1]), 0)};
+    for (int tile = grp; tile < num_tiles; tile += ngrp) {
+      const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
       const int n0 = (tile % args.num_n_blk) * GEMM_BN;
       const int r0 = m0 + quad * 32;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -276,7 +310,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // All TMEM reads of this accumulator are complete (tcgen05.wait::ld above).
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader[acc]);
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) tma_store_wait_all<0>();
@@ -284,33 +321,75 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    if constexpr (CG == 2) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
   }
 }
 
 
-int gemm_smem_bytes() { return GEMM_SMEM_BYTES; }
+int gemm_smem_bytes() { return GemmCfg<2>::SMEM; }
 
 static int g_num_sms = 0;
+static int g_gemm_cg = 0;
 
-template <int EPI>
+int gemm_cta_group() {
+  if (g_gemm_cg == 0) {
+    const char* e = getenv("PF_GEMM_CTAS");
+    g_gemm_cg = (e && e[0] == '1') ? 1 : 2;
+  }
+  return g_gemm_cg;
+}
+
+template <int EPI, int CG>
 static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                          const GemmArgs& a, cudaStream_t stream) {
+  using Cfg = GemmCfg<CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI, CG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return fail(-4, "gemm smem attr: %s", cudaGetErrorString(e));
     attr_set = true;
   }
   const int tiles = a.num_m_blk * a.num_n_blk;
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  gemm_bf16_kernel<EPI><<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(ta, tb, tc, a);
-  cudaError_t e = cudaGetLastError();
+  const int groups = g_num_sms / CG;
+  const int grid = (tiles < groups ? tiles : groups) * CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<EPI, CG>, ta, tb, tc, a);
+  if (e != cudaSuccess) return fail(-4, "gemm launch: %s", cudaGetErrorString(e));
+  e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "gemm launch: %s", cudaGetErrorString(e));
+}
+
+template <int CG>
+static int dispatch_gemm(const GemmDesc& d, const CUtensorMap& ta, const CUtensorMap& tb,
+                         const CUtensorMap& tc, GemmArgs a, cudaStream_t stream) {
+  a.num_m_blk = (d.M + GemmCfg<CG>::TILE_M - 1) / GemmCfg<CG>::TILE_M;
+  switch (d.epilogue) {
+    case EPI_BF16: return launch_gemm_t<EPI_BF16, CG>(ta, tb, tc, a, stream);
+    case EPI_ROPE_BF16: return launch_gemm_t<EPI_ROPE_BF16, CG>(ta, tb, tc, a, stream);
+    case EPI_SWIGLU: return launch_gemm_t<EPI_SWIGLU, CG>(ta, tb, tc, a, stream);
+    case EPI_RESID_ADD: return launch_gemm_t<EPI_RESID_ADD, CG>(ta, tb, tc, a, stream);
+    default: return fail(-2, "gemm: unknown epilogue %d", d.epilogue);
+  }
+}
+
+bool make_weight_tmap(CUtensorMap* out, const void* B, int N, int K, int ldb) {
+  return make_tmap_2d(out, B, 2, N, K, ldb, GEMM_BN / gemm_cta_group(), GEMM_BK, true);
 }
 
 int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t stream) {
@@ -326,10 +405,11 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  const int cg = gemm_cta_group();
   CUtensorMap ta, tb, tc;
   if (!make_tmap_2d(&ta, d.A, 2, d.M, d.K, d.lda, GEMM_BM, GEMM_BK, true)) return -3;
   if (cached_b) tb = *cached_b;
-  else if (!make_tmap_2d(&tb, d.B, 2, d.N, d.K, d.ldb, GEMM_BN, GEMM_BK, true)) return -3;
+  else if (!make_weight_tmap(&tb, d.B, d.N, d.K, d.ldb)) return -3;
   const int out_cols = d.epilogue == EPI_SWIGLU ? d.N / 2 : d.N;
   if (d.epilogue == EPI_RESID_ADD) {
     if (!make_tmap_2d(&tc, d.C, 4, d.M, out_cols, d.ldc, 32, 32, true)) return -3;
@@ -338,16 +418,9 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
   }
   GemmArgs a;
   a.M = d.M; a.N = d.N; a.K = d.K;
-  a.num_m_blk = (d.M + GEMM_BM - 1) / GEMM_BM;
   a.num_n_blk = (d.N + GEMM_BN - 1) / GEMM_BN;
   a.pos = d.pos; a.rope_cos = d.rope_cos; a.rope_sin = d.rope_sin; a.rope_heads = d.rope_heads;
-  switch (d.epilogue) {
-    case EPI_BF16: return launch_gemm_t<EPI_BF16>(ta, tb, tc, a, stream);
-    case EPI_ROPE_BF16: return launch_gemm_t<EPI_ROPE_BF16>(ta, tb, tc, a, stream);
-    case EPI_SWIGLU: return launch_gemm_t<EPI_SWIGLU>(ta, tb, tc, a, stream);
-    case EPI_RESID_ADD: return launch_gemm_t<EPI_RESID_ADD>(ta, tb, tc, a, stream);
-    default: return fail(-2, "gemm: unknown epilogue %d", d.epilogue);
-  }
+  return cg == 2 ? dispatch_gemm<2>(d, ta, tb, tc, a, stream) : dispatch_gemm<1>(d, ta, tb, tc, a, stream);
 }
 
 }  // namespace pf

@@ -42,6 +42,8 @@ struct GemmDesc {
 };
 int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t stream);
 int gemm_smem_bytes();
+int gemm_cta_group();   // 2 (default) or 1 via PF_GEMM_CTAS=1
+bool make_weight_tmap(CUtensorMap* out, const void* B, int N, int K, int ldb);
 
 int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, int T, int d, int vocab,
                  cudaStream_t stream);
