@@ -218,6 +218,9 @@ def run_ours(args):
     pp = PinnedPacked(packed)
     n_items = packed.n_items
     flops_step = algorithmic_flops(cfg, shape.prefix_len, [shape.suffix_len] * shape.n_items) * shape.n_requests
+    # executed work: the last layer's O-projection + MLP run on the n_items last-token rows only
+    flops_exec = flops_step - shape.n_requests * (packed.T // shape.n_requests - shape.n_items) * 2 * (
+        cfg.q_width * cfg.d_model + 3 * cfg.d_model * cfg.d_ff)
     launches_per_step = 2 + 7 * cfg.n_layers
 
     def barrier():
@@ -310,9 +313,11 @@ def run_ours(args):
         "data": "synthetic (seeded uniform token ids, <|ans|> last token; random-init bf16 weights)",
         "config": workload_config(args.config, cfg, shape, ws),
         "tok_per_s": packed.T * ws / (ms_step * 1e-3),
-        "step_tensor_frac": {"achieved_tflops": flops_step / (ms_step * 1e-3) / 1e12,
-                             "frac_of_sustained": flops_step / (ms_step * 1e-3) / 1e12 / peak_sust,
-                             "frac_of_burst": flops_step / (ms_step * 1e-3) / 1e12 / peak_burst,
+        "step_tensor_frac": {"achieved_tflops": flops_exec / (ms_step * 1e-3) / 1e12,
+                             "frac_of_sustained": flops_exec / (ms_step * 1e-3) / 1e12 / peak_sust,
+                             "frac_of_burst": flops_exec / (ms_step * 1e-3) / 1e12 / peak_burst,
+                             "flops_per_step_executed": flops_exec,
+                             "flops_per_step_all_rows": flops_step,
                              "peak_kind": peak_kind},
         "e2e": {"value": e2e_val, "unit": "items/s", "h2d_bytes_per_step": pp.h2d_bytes(),
                 "d2h_bytes_per_step": pp.d2h_bytes(), "ms_per_step": e2e_s / args.steps * 1e3},

@@ -40,7 +40,9 @@ typedef struct pf_model pf_model;        /* opaque: config + cached weight TMA d
  *   w_o[l]     bf16 [d_model x n_heads d_head]
  *   w_gu[l]    bf16 [2 d_ff_pad x d_model]   per 128-neuron block j: 128 gate rows then 128 up rows
  *   w_down[l]  bf16 [d_model x d_ff_pad]     columns >= d_ff are zero (pruned/padded neurons)
- *   ln_attn[l], ln_mlp[l], ln_final : fp32 [d_model] RMSNorm scales
+ *   The per-layer RMSNorm gains are FOLDED into the GEMM input rows (RMSNorm is fused into the
+ *   GEMM epilogues): w_qkv[l] = (diag(g_attn[l]) W_qkv)^T and w_gu[l] = (diag(g_mlp[l]) W_gu)^T.
+ *   ln_final : fp32 [d_model] final RMSNorm scale (applied in the head kernel)
  *   w_yes, w_no: fp32 [d_model] — columns yes_id / no_id of the [d_model x vocab] output head
  *   rope_cos, rope_sin: fp32 [max_seq x d_head/2]  (theta^(-2i/d_head) * pos, rotate-half)
  */
@@ -52,8 +54,6 @@ typedef struct pf_model_desc {
   const void* const* w_o;
   const void* const* w_gu;
   const void* const* w_down;
-  const float* const* ln_attn;
-  const float* const* ln_mlp;
   const float* ln_final;
   const float* w_yes;
   const float* w_no;
@@ -96,11 +96,23 @@ PF_API int pf_score_host(pf_model* model, const int32_t* ids, const int32_t* pos
 
 /* Per-op entry points (unit parity tests). */
 /* C = A[MxK] . B[NxK]^T with epilogue 0 bf16, 1 bf16+RoPE, 2 SwiGLU(bf16, N/2 cols),
- * 3 fp32 C += (residual add). */
+ * 3 fp32 C += (residual add), 4 fp32 C += acc with xb = bf16(C) and ss_out[row] += sum(C^2). */
 PF_API int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
                  int K, int epilogue, const int32_t* pos, const float* rope_cos,
                  const float* rope_sin, int rope_heads, pf_stream_t stream);
-PF_API int pf_embed(const int32_t* ids, const void* emb, float* resid, int T, int d, pf_stream_t stream);
+/* Full-option GEMM (fused RMSNorm): row_ss != NULL scales accumulator row r by
+ * rsqrt(row_ss[r] * inv_d + eps); ss_zero rows are cleared by the n-tile-0 CTAs. */
+typedef struct pf_gemm_args {
+  const void* A; int lda; const void* B; int ldb; void* C; int ldc;
+  int M, N, K, epilogue;
+  const int32_t* pos; const float* rope_cos; const float* rope_sin; int rope_heads;
+  const float* row_ss; float* ss_zero; float* ss_out; void* xb; int ldxb; float inv_d, eps;
+} pf_gemm_args;
+PF_API int pf_gemm_bf16_ex(const pf_gemm_args* args, pf_stream_t stream);
+/* resid = float(E[ids]); optional xb = E[ids] (bf16) and ss = per-row sum of squares. */
+PF_API int pf_embed(const int32_t* ids, const void* emb, float* resid, void* xb, float* ss, int T, int d,
+             pf_stream_t stream);
+/* y = bf16(x * rsqrt(mean(x^2) + eps) * gamma); gamma may be NULL (all ones). */
 PF_API int pf_rmsnorm(const float* x, const float* gamma, void* y_bf16, int T, int d, float eps,
                pf_stream_t stream);
 PF_API int pf_prefix_attention(const void* qkv, void* out, int T, int n_heads, int n_kv_heads,

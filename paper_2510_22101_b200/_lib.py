@@ -16,12 +16,12 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libprefill_
 # Error codes (include/prefill_sm100.h)
 PF_EARG, PF_ESHAPE, PF_ETMAP, PF_ECUDA, PF_EWORKSPACE, PF_ENONFINITE = -1, -2, -3, -4, -5, -6
 
-EPI_BF16, EPI_ROPE_BF16, EPI_SWIGLU, EPI_RESID_ADD = 0, 1, 2, 3
+EPI_BF16, EPI_ROPE_BF16, EPI_SWIGLU, EPI_RESID_ADD, EPI_RESID_ADD_NORM = 0, 1, 2, 3, 4
 
 # Every symbol include/prefill_sm100.h declares (tests check the .so exports all of them).
 EXPORTED_SYMBOLS = (
     "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host",
-    "pf_gemm_bf16", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
+    "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
     "pf_last_error", "pf_version",
 )
 
@@ -49,13 +49,23 @@ class PfModelDesc(ctypes.Structure):
         ("w_o", ctypes.POINTER(ctypes.c_void_p)),
         ("w_gu", ctypes.POINTER(ctypes.c_void_p)),
         ("w_down", ctypes.POINTER(ctypes.c_void_p)),
-        ("ln_attn", ctypes.POINTER(ctypes.c_void_p)),
-        ("ln_mlp", ctypes.POINTER(ctypes.c_void_p)),
         ("ln_final", ctypes.c_void_p),
         ("w_yes", ctypes.c_void_p),
         ("w_no", ctypes.c_void_p),
         ("rope_cos", ctypes.c_void_p),
         ("rope_sin", ctypes.c_void_p),
+    ]
+
+
+class PfGemmArgs(ctypes.Structure):
+    _fields_ = [
+        ("A", ctypes.c_void_p), ("lda", ctypes.c_int), ("B", ctypes.c_void_p), ("ldb", ctypes.c_int),
+        ("C", ctypes.c_void_p), ("ldc", ctypes.c_int),
+        ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int), ("epilogue", ctypes.c_int),
+        ("pos", ctypes.c_void_p), ("rope_cos", ctypes.c_void_p), ("rope_sin", ctypes.c_void_p),
+        ("rope_heads", ctypes.c_int),
+        ("row_ss", ctypes.c_void_p), ("ss_zero", ctypes.c_void_p), ("ss_out", ctypes.c_void_p),
+        ("xb", ctypes.c_void_p), ("ldxb", ctypes.c_int), ("inv_d", ctypes.c_float), ("eps", ctypes.c_float),
     ]
 
 
@@ -71,7 +81,8 @@ _SIGS = {
     "pf_score": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "pf_score_host": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P]),
     "pf_gemm_bf16": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),
-    "pf_embed": (_I, [_P, _P, _P, _I, _I, _P]),
+    "pf_gemm_bf16_ex": (_I, [ctypes.POINTER(PfGemmArgs), _P]),
+    "pf_embed": (_I, [_P, _P, _P, _P, _P, _I, _I, _P]),
     "pf_rmsnorm": (_I, [_P, _P, _P, _I, _I, _F, _P]),
     "pf_prefix_attention": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _I, _P]),
     "pf_head_last_token": (_I, [_P, _P, _I, _I, _P, _P, _P, _F, _P, _P, _P, _P]),

@@ -2,6 +2,7 @@
 // the packed forward (pf_score), the host-buffer variant and per-op entry points.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -74,9 +75,9 @@ using namespace pf;
 struct pf_model {
   pf_model_desc d;
   std::vector<const void*> w_qkv, w_o, w_gu, w_down;
-  std::vector<const float*> ln_attn, ln_mlp;
   std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;  // cached weight (B operand) maps
   int qkv_n, attn_k;
+  bool last_layer_compact;   // PF_NO_LAST_LAYER_COMPACT=1 disables (for tests/benchmarks)
 };
 
 namespace {
@@ -86,10 +87,14 @@ size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Workspace {
   float* resid;
-  void* xn;
+  void* xb;          // bf16(residual) = A operand of QKV / gate-up (norm applied in epilogue)
+  float* ss_attn;    // per-row sum of squares of the residual feeding the attention block
+  float* ss_mlp;     // ... feeding the MLP block
   void* qkv;
   void* attn;
   void* hbuf;
+  void* attn_c;      // [n_items x H*dh] bf16  last-layer compacted rows
+  float* resid_c;    // [n_items x d] fp32
   // device copies of host inputs/outputs (pf_score_host)
   int32_t *ids, *pos, *segs, *work, *last_idx;
   float *logits2, *p_yes;
@@ -103,10 +108,14 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   size_t off = 0;
   auto take = [&](size_t bytes) { uint8_t* p = base + off; off = align_up(off + bytes); return p; };
   w.resid = reinterpret_cast<float*>(take((size_t)T * d.d_model * 4));
-  w.xn = take((size_t)T * d.d_model * 2);
+  w.xb = take((size_t)T * d.d_model * 2);
+  w.ss_attn = reinterpret_cast<float*>(take((size_t)T * 4));
+  w.ss_mlp = reinterpret_cast<float*>(take((size_t)T * 4));
   w.qkv = take((size_t)T * m->qkv_n * 2);
   w.attn = take((size_t)T * m->attn_k * 2);
   w.hbuf = take((size_t)T * d.d_ff_pad * 2);
+  w.attn_c = take((size_t)n_items * m->attn_k * 2);
+  w.resid_c = reinterpret_cast<float*>(take((size_t)n_items * d.d_model * 4));
   w.ids = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.pos = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.segs = reinterpret_cast<int32_t*>(take((size_t)n_seg * 16));
@@ -141,19 +150,19 @@ int pf_model_create(const pf_model_desc* desc, pf_model** out) {
   m->d = d;
   m->qkv_n = (d.n_heads + 2 * d.n_kv_heads) * d.d_head;
   m->attn_k = d.n_heads * d.d_head;
+  {
+    const char* e = getenv("PF_NO_LAST_LAYER_COMPACT");
+    m->last_layer_compact = !(e && e[0] == '1');
+  }
   const int L = d.n_layers;
   m->w_qkv.assign(d.w_qkv, d.w_qkv + L);
   m->w_o.assign(d.w_o, d.w_o + L);
   m->w_gu.assign(d.w_gu, d.w_gu + L);
   m->w_down.assign(d.w_down, d.w_down + L);
-  m->ln_attn.assign(d.ln_attn, d.ln_attn + L);
-  m->ln_mlp.assign(d.ln_mlp, d.ln_mlp + L);
   m->d.w_qkv = m->w_qkv.data();
   m->d.w_o = m->w_o.data();
   m->d.w_gu = m->w_gu.data();
   m->d.w_down = m->w_down.data();
-  m->d.ln_attn = m->ln_attn.data();
-  m->d.ln_mlp = m->ln_mlp.data();
   m->tm_qkv.resize(L);
   m->tm_o.resize(L);
   m->tm_gu.resize(L);
@@ -187,35 +196,62 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
   (void)n_seg;
   const pf_model_desc& d = m->d;
   const float eps = d.rms_eps;
-  int rc = launch_embed(ids, d.embedding, w.resid, T, d.d_model, d.vocab_size, st);
+  const float inv_d = 1.0f / (float)d.d_model;
+  // Fused RMSNorm: the residual-update epilogues keep xb = bf16(resid) and ss = sum(resid^2);
+  // the next GEMM scales its accumulator rows by rsqrt(ss/d + eps) (norm gains are folded into
+  // w_qkv / w_gu by the caller, include/prefill_sm100.h).
+  int rc = launch_embed(ids, d.embedding, w.resid, w.xb, w.ss_attn, T, d.d_model, st);
   if (rc) return rc;
   for (int l = 0; l < d.n_layers; ++l) {
-    if ((rc = launch_rmsnorm(w.resid, d.ln_attn[l], w.xn, T, d.d_model, eps, st))) return rc;
     GemmDesc g{};
-    g.A = w.xn; g.lda = d.d_model; g.B = d.w_qkv[l]; g.ldb = d.d_model;
+    g.A = w.xb; g.lda = d.d_model; g.B = d.w_qkv[l]; g.ldb = d.d_model;
     g.C = w.qkv; g.ldc = m->qkv_n; g.M = T; g.N = m->qkv_n; g.K = d.d_model;
     g.epilogue = EPI_ROPE_BF16; g.pos = pos; g.rope_cos = d.rope_cos; g.rope_sin = d.rope_sin;
     g.rope_heads = d.n_heads + d.n_kv_heads; g.max_seq = d.max_seq;
+    g.row_ss = w.ss_attn; g.ss_zero = w.ss_mlp; g.inv_d = inv_d; g.eps = eps;
     if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
     AttnDesc a{};
     a.qkv = w.qkv; a.out = w.attn; a.T = T; a.H = d.n_heads; a.Hkv = d.n_kv_heads; a.dh = d.d_head;
     a.work = work; a.n_work = n_work; a.segs = segs; a.scale = 1.0f / sqrtf((float)d.d_head);
     if ((rc = launch_attention(a, st))) return rc;
+    if (l == d.n_layers - 1 && n_items < T && m->last_layer_compact) {
+      // Last layer: only the n_items last-token rows reach the head, so the O-projection and MLP
+      // run on those rows alone (per-row arithmetic unchanged; tests check bit-equality).
+      if ((rc = launch_gather_rows(last_idx, n_items, w.attn, m->attn_k, w.resid, d.d_model, w.attn_c,
+                                   w.resid_c, st)))
+        return rc;
+      GemmDesc o{};
+      o.A = w.attn_c; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
+      o.C = w.resid_c; o.ldc = d.d_model; o.M = n_items; o.N = d.d_model; o.K = m->attn_k;
+      o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp;
+      if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
+      GemmDesc gu{};
+      gu.A = w.xb; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
+      gu.C = w.hbuf; gu.ldc = d.d_ff_pad; gu.M = n_items; gu.N = 2 * d.d_ff_pad; gu.K = d.d_model;
+      gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.inv_d = inv_d; gu.eps = eps;
+      if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
+      GemmDesc dn{};
+      dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
+      dn.C = w.resid_c; dn.ldc = d.d_model; dn.M = n_items; dn.N = d.d_model; dn.K = d.d_ff_pad;
+      dn.epilogue = EPI_RESID_ADD;
+      if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
+      return launch_head(w.resid_c, nullptr, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
+                         logits2, p_yes, bad, st);
+    }
     GemmDesc o{};
     o.A = w.attn; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
     o.C = w.resid; o.ldc = d.d_model; o.M = T; o.N = d.d_model; o.K = m->attn_k;
-    o.epilogue = EPI_RESID_ADD;
+    o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp;
     if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
-    if ((rc = launch_rmsnorm(w.resid, d.ln_mlp[l], w.xn, T, d.d_model, eps, st))) return rc;
     GemmDesc gu{};
-    gu.A = w.xn; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
+    gu.A = w.xb; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
     gu.C = w.hbuf; gu.ldc = d.d_ff_pad; gu.M = T; gu.N = 2 * d.d_ff_pad; gu.K = d.d_model;
-    gu.epilogue = EPI_SWIGLU;
+    gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.ss_zero = w.ss_attn; gu.inv_d = inv_d; gu.eps = eps;
     if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
     GemmDesc dn{};
     dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
     dn.C = w.resid; dn.ldc = d.d_model; dn.M = T; dn.N = d.d_model; dn.K = d.d_ff_pad;
-    dn.epilogue = EPI_RESID_ADD;
+    dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.xb; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn;
     if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
   }
   return launch_head(w.resid, last_idx, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
@@ -285,8 +321,20 @@ int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ld
   return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int pf_embed(const int32_t* ids, const void* emb, float* resid, int T, int d, pf_stream_t stream) {
-  return launch_embed(ids, emb, resid, T, d, 0, reinterpret_cast<cudaStream_t>(stream));
+int pf_embed(const int32_t* ids, const void* emb, float* resid, void* xb, float* ss, int T, int d,
+             pf_stream_t stream) {
+  return launch_embed(ids, emb, resid, xb, ss, T, d, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_gemm_bf16_ex(const pf_gemm_args* a, pf_stream_t stream) {
+  if (!a) return fail(-1, "pf_gemm_bf16_ex: null args");
+  GemmDesc g{};
+  g.A = a->A; g.lda = a->lda; g.B = a->B; g.ldb = a->ldb; g.C = a->C; g.ldc = a->ldc;
+  g.M = a->M; g.N = a->N; g.K = a->K; g.epilogue = a->epilogue;
+  g.pos = a->pos; g.rope_cos = a->rope_cos; g.rope_sin = a->rope_sin; g.rope_heads = a->rope_heads;
+  g.row_ss = a->row_ss; g.ss_zero = a->ss_zero; g.ss_out = a->ss_out; g.xb = a->xb; g.ldxb = a->ldxb;
+  g.inv_d = a->inv_d; g.eps = a->eps;
+  return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int pf_rmsnorm(const float* x, const float* gamma, void* y, int T, int d, float eps, pf_stream_t stream) {

@@ -17,16 +17,19 @@ PF_DEVICE float warp_sum(float v) {
 }
 
 // ---------------------------------------------------------------- embedding gather
-// VPL = bf16 uint4 (8 values) per lane: d = VPL * 256.
+// x[t] = float(E[id[t]]) (fp32 residual stream); optionally also xb[t] = E[id[t]] (the bf16 A
+// operand of layer 0's QKV GEMM) and ss[t] = sum(x^2) (its fused RMSNorm statistic).
 __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ ids,
                                                     const __nv_bfloat16* __restrict__ emb,
-                                                    float* __restrict__ resid, int T, int d) {
+                                                    float* __restrict__ resid, uint4* __restrict__ xb,
+                                                    float* __restrict__ ss, int T, int d) {
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
   const int id = __ldg(ids + t);
   const uint4* src = reinterpret_cast<const uint4*>(emb + (size_t)id * d);
   float4* dst = reinterpret_cast<float4*>(resid + (size_t)t * d);
+  float acc = 0.f;
   for (int i = lane; i < d / 8; i += 32) {
     const uint4 u = __ldg(src + i);
     const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -34,6 +37,12 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ 
     const float2 c = __bfloat1622float2(p[2]), e = __bfloat1622float2(p[3]);
     dst[2 * i] = make_float4(a.x, a.y, b.x, b.y);
     dst[2 * i + 1] = make_float4(c.x, c.y, e.x, e.y);
+    if (xb) xb[(size_t)t * (d / 8) + i] = u;
+    acc += a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y + c.x * c.x + c.y * c.y + e.x * e.x + e.y * e.y;
+  }
+  if (ss) {
+    acc = warp_sum(acc);
+    if (lane == 0) ss[t] = acc;
   }
 }
 
@@ -63,7 +72,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
   uint2* dst = reinterpret_cast<uint2*>(y + (size_t)t * d);
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    const float4 gg = __ldg(g4 + lane + 32 * i);
+    const float4 gg = g4 ? __ldg(g4 + lane + 32 * i) : make_float4(1.f, 1.f, 1.f, 1.f);
     uint2 o;
     o.x = pack_bf16x2(v[i].x * r * gg.x, v[i].y * r * gg.y);
     o.y = pack_bf16x2(v[i].z * r * gg.z, v[i].w * r * gg.w);
@@ -84,7 +93,7 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ res
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n_items) return;
-  const float* x = resid + (size_t)__ldg(last_idx + i) * d;
+  const float* x = resid + (size_t)(last_idx ? __ldg(last_idx + i) : i) * d;
   float ss = 0.f;
   for (int j = lane; j < d; j += 32) { const float v = x[j]; ss += v * v; }
   ss = warp_sum(ss);
@@ -105,13 +114,37 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ res
   }
 }
 
-int launch_embed(const int32_t* ids, const void* emb, float* resid, int T, int d, int vocab,
+// ---------------------------------------------------------------- last-row gather
+// Compacts the rows the head needs (one per item) before the last layer's O-projection + MLP:
+// attn_c[i] = attn[last_idx[i]] (bf16), resid_c[i] = resid[last_idx[i]] (fp32).
+__global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restrict__ last_idx, int n,
+                                                          const uint4* __restrict__ attn, int attn_v4,
+                                                          const float4* __restrict__ resid, int resid_v4,
+                                                          uint4* __restrict__ attn_c, float4* __restrict__ resid_c) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const size_t r = (size_t)__ldg(last_idx + i);
+  for (int j = lane; j < attn_v4; j += 32) attn_c[(size_t)i * attn_v4 + j] = __ldg(attn + r * attn_v4 + j);
+  for (int j = lane; j < resid_v4; j += 32) resid_c[(size_t)i * resid_v4 + j] = __ldg(resid + r * resid_v4 + j);
+}
+
+int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const float* resid,
+                       int d, void* attn_c, float* resid_c, cudaStream_t stream) {
+  if (n == 0) return 0;
+  gather_rows_kernel<<<(n + 7) / 8, 256, 0, stream>>>(
+      last_idx, n, reinterpret_cast<const uint4*>(attn), attn_cols / 8, reinterpret_cast<const float4*>(resid),
+      d / 4, reinterpret_cast<uint4*>(attn_c), reinterpret_cast<float4*>(resid_c));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "gather launch: %s", cudaGetErrorString(e));
+}
+
+int launch_embed(const int32_t* ids, const void* emb, float* resid, void* xb, float* ss, int T, int d,
                  cudaStream_t stream) {
-  (void)vocab;
   if (d % 8 != 0) return fail(-2, "embed: d_model must be a multiple of 8");
   if (T == 0) return 0;
   embed_kernel<<<(T + 7) / 8, 256, 0, stream>>>(ids, reinterpret_cast<const __nv_bfloat16*>(emb),
-                                                resid, T, d);
+                                                resid, reinterpret_cast<uint4*>(xb), ss, T, d);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "embed launch: %s", cudaGetErrorString(e));
 }

@@ -31,13 +31,19 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 // CG = CTAs per MMA (cta_group).  CG=2: a CTA pair computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 (M=256); each CTA loads its own 128 A rows and half (128) of the
 // B rows, so per-CTA operand bytes per MMA drop from 48 KB to 32 KB per k-block.
-template <int CG>
+// EPI_RESID_ADD_NORM reads the old residual through a per-warp ring of RB_DEPTH TMA-loaded
+// 32x32 fp32 chunks (4 KB each), so it trades two mainloop stages for that ring.
+constexpr int RB_DEPTH = 4;
+template <int CG, int EPI>
 struct GemmCfg {
   static constexpr int B_ROWS = GEMM_BN / CG;                // B rows loaded per CTA
   static constexpr int B_BYTES = B_ROWS * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 4 * 2 * GEMM_STG_BYTES + 256;
+  static constexpr bool RING = EPI == EPI_RESID_ADD_NORM;
+  static constexpr int STAGES = RING ? 4 : (CG == 2 ? 6 : 4);
+  // ring: RB_DEPTH fp32 chunk buffers + 2 bf16 staging boxes per epilogue warp
+  static constexpr int EPI_BYTES = RING ? 4 * (RB_DEPTH + 2) * GEMM_STG_BYTES : 4 * 2 * GEMM_STG_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
   static constexpr int TILE_M = GEMM_BM * CG;
 };
 
@@ -48,7 +54,23 @@ struct GemmArgs {
   const float* rope_cos;   // [max_seq x 64]
   const float* rope_sin;
   int rope_heads;          // heads (of 128 cols) that receive RoPE
+  const float* row_ss;     // fused RMSNorm: per-row sum of squares of the residual (or null)
+  float* ss_zero;          // rows to clear (n-tile 0) for the next accumulation (or null)
+  float* ss_out;           // EPI_RESID_ADD_NORM: per-row sum of squares accumulator
+  const float* resid;      // EPI_RESID_ADD_NORM: residual base pointer (== C)
+  int ldr;
+  void* xb_out;            // EPI_RESID_ADD_NORM: bf16 copy of the new residual
+  int ldxb;
+  float inv_d, eps;
 };
+
+PF_DEVICE float4 ldg_cg_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
 
 PF_DEVICE float silu(float g) { return g / (1.0f + __expf(-g)); }
 
@@ -64,19 +86,21 @@ PF_DEVICE void stage_row_128B(uint32_t stg, uint32_t row, const uint32_t (&w)[32
 template <int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
-  using Cfg = GemmCfg<CG>;
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
+                     const GemmArgs args) {
+  using Cfg = GemmCfg<CG, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::STAGES * GEMM_A_BYTES;
   uint8_t* sStg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 2 * GEMM_STG_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + Cfg::EPI_BYTES);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + Cfg::STAGES;
   uint64_t* tfull_bar = bars + 2 * Cfg::STAGES;
   uint64_t* tempty_bar = bars + 2 * Cfg::STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4);
+  uint64_t* rbar = bars + 2 * Cfg::STAGES + 4;            // [4 warps][RB_DEPTH] (ring epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4 + 4 * RB_DEPTH);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -100,6 +124,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4 * CG);   // every epilogue warp of the group arrives
     }
+    if constexpr (Cfg::RING)
+      for (int i = 0; i < 4 * RB_DEPTH; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -175,14 +201,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // -------------------------------------------------------------- epilogue (warps 2..5)
     const uint32_t quad = warp & 3;          // TMEM lane quadrant this warp may access
     const uint32_t row = quad * 32 + lane;   // row within the 128-row tile
-    uint8_t* my_stg = sStg + (warp - 2) * 2 * GEMM_STG_BYTES;
+    uint8_t* my_stg = sStg + (warp - 2) * (Cfg::EPI_BYTES / 4);
     int stg_idx = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
 
     // Stage one 32x128B box and launch its TMA store / reduce. Buffers alternate; the wait
     // keeps at most one store per warp in flight against the buffer being overwritten.
-    auto emit = [&](const uint32_t (&w)[32], int c0, int r0) {
+    auto emit_to = [&](const uint32_t (&w)[32], int c0, int r0, const CUtensorMap* map, bool reduce) {
       if (lane == 0) tma_store_wait_read<1>();
       __syncwarp();
       const uint32_t stg = smem_u32(my_stg + stg_idx * GEMM_STG_BYTES);
@@ -190,16 +216,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (EPI == EPI_RESID_ADD) tma_reduce_add_2d(&tmC, my_stg + stg_idx * GEMM_STG_BYTES, c0, r0);
-        else tma_store_2d(&tmC, my_stg + stg_idx * GEMM_STG_BYTES, c0, r0);
+        if (reduce) tma_reduce_add_2d(map, my_stg + stg_idx * GEMM_STG_BYTES, c0, r0);
+        else tma_store_2d(map, my_stg + stg_idx * GEMM_STG_BYTES, c0, r0);
         tma_store_commit();
       }
       stg_idx ^= 1;
     };
+    auto emit = [&](const uint32_t (&w)[32], int c0, int r0) {
+      emit_to(w, c0, r0, &tmC, EPI == EPI_RESID_ADD);
+    };
 
-    // the MMA issuer waits on the leader's tmem-empty barrier
-    const uint32_t tempty_leader[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0),
-                                       mapa_shared(smem_u32(&tempty_bar[1]), 0)};
+    // ---- EPI_RESID_ADD_NORM residual ring: chunk k of this warp lives in buffer k % RB_DEPTH
+    uint64_t* my_rbar = rbar + (warp - 2) * RB_DEPTH;
+    uint32_t ring_issued = 0, ring_used = 0;
+    auto ring_issue = [&](int t, int c) {   // TMA-load chunk c (32 cols) of tile t's 32 rows
+      const int mm = (t / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM + quad * 32;
+      const int nn = (t % args.num_n_blk) * GEMM_BN + c * 32;
+      const uint32_t b = ring_issued % RB_DEPTH;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&my_rbar[b], GEMM_STG_BYTES);
+        tma_load_2d(my_stg + b * GEMM_STG_BYTES, &tmC, &my_rbar[b], nn, mm, kEvictFirst);
+      }
+      ++ring_issued;
+    };
+    auto ring_chunks = [&](int t) { return min(GEMM_BN / 32, (args.N - (t % args.num_n_blk) * GEMM_BN) / 32); };
+    if constexpr (Cfg::RING) {
+      if (grp < num_tiles)
+        for (int c = 0; c < min(RB_DEPTH, ring_chunks(grp)); ++c) ring_issue(grp, c);
+    }
     for (int tile = grp; tile < num_tiles; tile += ngrp) {
       const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
       const int n0 = (tile % args.num_n_blk) * GEMM_BN;
@@ -207,6 +251,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * GEMM_BN;
+      const int grow = m0 + (int)row;
+      const bool rvalid = grow < args.M;
+      // fused RMSNorm: the A rows were bf16(residual); scale the accumulator row by rstd
+      float rs = 1.f;
+      if (args.row_ss != nullptr && rvalid) rs = rsqrtf(__ldg(args.row_ss + grow) * args.inv_d + args.eps);
+      if (args.ss_zero != nullptr && rvalid && (tile % args.num_n_blk) == 0) args.ss_zero[grow] = 0.f;
 
       if constexpr (EPI == EPI_BF16) {
 #pragma unroll 1
@@ -217,8 +267,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            w[i] = pack_bf16x2(__uint_as_float(v0[2 * i]), __uint_as_float(v0[2 * i + 1]));
-            w[16 + i] = pack_bf16x2(__uint_as_float(v1[2 * i]), __uint_as_float(v1[2 * i + 1]));
+            w[i] = pack_bf16x2(__uint_as_float(v0[2 * i]) * rs, __uint_as_float(v0[2 * i + 1]) * rs);
+            w[16 + i] = pack_bf16x2(__uint_as_float(v1[2 * i]) * rs, __uint_as_float(v1[2 * i + 1]) * rs);
           }
           emit(w, n0 + c * 64, r0);
         }
@@ -229,6 +279,75 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_ld_32x32b_x32(t_row + c * 32, v);
           tmem_ld_wait();
           emit(v, n0 + c * 32, r0);
+        }
+      } else if constexpr (EPI == EPI_RESID_ADD_NORM) {
+        // new = old + acc (fp32) -> resid;  bf16(new) -> xb (next GEMM's A operand);
+        // ss_out[row] += sum(new^2) (next RMSNorm).  Old residual chunks arrive by TMA into a
+        // per-warp ring (the first RB_DEPTH issued while this tile's MMAs ran); the new values
+        // overwrite the chunk in place and leave by TMA store, the bf16 copy through a 64-column
+        // staging box.  Bulk-group accounting: iteration k commits G_f(k) and, for odd k, G_b(k).
+        const int n_chunks = ring_chunks(tile);
+        uint8_t* bf_stg = my_stg + RB_DEPTH * GEMM_STG_BYTES;
+        float ssq = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < n_chunks; ++c) {
+          const uint32_t k = ring_used;
+          const uint32_t b = k % RB_DEPTH;
+          // G_f(k-2) has exactly two later groups: once it has been read, chunk k-2's buffer can be
+          // refilled and (for even c) the bf16 box last stored as G_b(k-3) can be rewritten.
+          if (c >= 2) {
+            if (lane == 0) tma_store_wait_read<2>();
+            __syncwarp();
+            if (c + 2 < n_chunks) ring_issue(tile, c + 2);
+          }
+          mbar_wait(&my_rbar[b], (k / RB_DEPTH) & 1);
+          ++ring_used;
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, v);
+          const uint32_t rrow = smem_u32(my_stg + b * GEMM_STG_BYTES) + lane * 128;
+          const uint32_t brow = smem_u32(bf_stg + ((c >> 1) & 1) * GEMM_STG_BYTES) + lane * 128;
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t addr = rrow + ((j ^ (lane & 7)) << 4);
+            float4 o;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w) : "r"(addr));
+            o.x += __uint_as_float(v[4 * j]);
+            o.y += __uint_as_float(v[4 * j + 1]);
+            o.z += __uint_as_float(v[4 * j + 2]);
+            o.w += __uint_as_float(v[4 * j + 3]);
+            ssq += o.x * o.x + o.y * o.y + o.z * o.z + o.w * o.w;
+            st_shared_v4(addr, __float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z),
+                         __float_as_uint(o.w));
+            const uint32_t p0 = pack_bf16x2(o.x, o.y), p1 = pack_bf16x2(o.z, o.w);
+            // bf16: 32 fp32 cols = 64 B = 16 B chunks [(c&1)*4, (c&1)*4+4) of the 128 B row
+            if (j & 1) {
+              asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(brow + ((((c & 1) * 4 + (j >> 1)) ^ (lane & 7)) << 4) + 8),
+                           "r"(p0), "r"(p1) : "memory");
+            } else {
+              asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(brow + ((((c & 1) * 4 + (j >> 1)) ^ (lane & 7)) << 4)),
+                           "r"(p0), "r"(p1) : "memory");
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, my_stg + b * GEMM_STG_BYTES, n0 + c * 32, r0);
+            tma_store_commit();
+            if (c & 1) {
+              tma_store_2d(&tmD, bf_stg + ((c >> 1) & 1) * GEMM_STG_BYTES, n0 + (c >> 1) * 64, r0);
+              tma_store_commit();
+            }
+          }
+        }
+        if (rvalid) atomicAdd(args.ss_out + grow, ssq);
+        // start the next tile's residual loads now; they land while its MMAs run
+        const int nt = tile + ngrp;
+        if (nt < num_tiles) {
+          if (lane == 0) tma_store_wait_read<0>();
+          __syncwarp();
+          for (int c = 0; c < min(RB_DEPTH, ring_chunks(nt)); ++c) ring_issue(nt, c);
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
         // B tile rows [0,128) = gate neurons, [128,256) = matching up neurons.
@@ -243,8 +362,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
-              float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+              float a0 = silu(__uint_as_float(g[2 * i]) * rs) * (__uint_as_float(u[2 * i]) * rs);
+              float a1 = silu(__uint_as_float(g[2 * i + 1]) * rs) * (__uint_as_float(u[2 * i + 1]) * rs);
               w[h * 16 + i] = pack_bf16x2(a0, a1);
             }
           }
@@ -254,8 +373,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // Rotate-half RoPE: head column i pairs with i+64.  For each 32-column half c the thread
         // loads x1 = cols [32c, 32c+32) and x2 = cols [64+32c, ...); rotated x1 lands in the
         // "lo" 64-col box (16-byte chunks 4c..4c+3), rotated x2 in the "hi" box.
-        const int grow = m0 + row;
-        const int p = (grow < args.M) ? __ldg(args.pos + grow) : 0;
+        const int p = rvalid ? __ldg(args.pos + grow) : 0;
         const float4* cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * 64);
         const float4* sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * 64);
         const uint32_t stg_lo = smem_u32(my_stg);
@@ -281,8 +399,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               float o1[4], o2[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float a = __uint_as_float(x1[j4 * 4 + e]);
-                const float b = __uint_as_float(x2[j4 * 4 + e]);
+                const float a = __uint_as_float(x1[j4 * 4 + e]) * rs;
+                const float b = __uint_as_float(x2[j4 * 4 + e]) * rs;
                 o1[e] = a * cc[e] - b * ss[e];
                 o2[e] = b * cc[e] + a * ss[e];
               }
@@ -311,7 +429,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader[acc]);
+        // the MMA issuer waits on the leader CTA's tmem-empty barrier
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
         else mbar_arrive(&tempty_bar[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -330,7 +449,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 
-int gemm_smem_bytes() { return GemmCfg<2>::SMEM; }
+int gemm_smem_bytes() { return GemmCfg<2, EPI_BF16>::SMEM; }
 
 static int g_num_sms = 0;
 static int g_gemm_cg = 0;
@@ -345,8 +464,8 @@ int gemm_cta_group() {
 
 template <int EPI, int CG>
 static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                         const GemmArgs& a, cudaStream_t stream) {
-  using Cfg = GemmCfg<CG>;
+                         const CUtensorMap& td, const GemmArgs& a, cudaStream_t stream) {
+  using Cfg = GemmCfg<CG, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI, CG>,
@@ -369,7 +488,7 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<EPI, CG>, ta, tb, tc, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<EPI, CG>, ta, tb, tc, td, a);
   if (e != cudaSuccess) return fail(-4, "gemm launch: %s", cudaGetErrorString(e));
   e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "gemm launch: %s", cudaGetErrorString(e));
@@ -377,13 +496,14 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
 
 template <int CG>
 static int dispatch_gemm(const GemmDesc& d, const CUtensorMap& ta, const CUtensorMap& tb,
-                         const CUtensorMap& tc, GemmArgs a, cudaStream_t stream) {
-  a.num_m_blk = (d.M + GemmCfg<CG>::TILE_M - 1) / GemmCfg<CG>::TILE_M;
+                         const CUtensorMap& tc, const CUtensorMap& td, GemmArgs a, cudaStream_t stream) {
+  a.num_m_blk = (d.M + GemmCfg<CG, EPI_BF16>::TILE_M - 1) / GemmCfg<CG, EPI_BF16>::TILE_M;
   switch (d.epilogue) {
-    case EPI_BF16: return launch_gemm_t<EPI_BF16, CG>(ta, tb, tc, a, stream);
-    case EPI_ROPE_BF16: return launch_gemm_t<EPI_ROPE_BF16, CG>(ta, tb, tc, a, stream);
-    case EPI_SWIGLU: return launch_gemm_t<EPI_SWIGLU, CG>(ta, tb, tc, a, stream);
-    case EPI_RESID_ADD: return launch_gemm_t<EPI_RESID_ADD, CG>(ta, tb, tc, a, stream);
+    case EPI_BF16: return launch_gemm_t<EPI_BF16, CG>(ta, tb, tc, td, a, stream);
+    case EPI_ROPE_BF16: return launch_gemm_t<EPI_ROPE_BF16, CG>(ta, tb, tc, td, a, stream);
+    case EPI_SWIGLU: return launch_gemm_t<EPI_SWIGLU, CG>(ta, tb, tc, td, a, stream);
+    case EPI_RESID_ADD: return launch_gemm_t<EPI_RESID_ADD, CG>(ta, tb, tc, td, a, stream);
+    case EPI_RESID_ADD_NORM: return launch_gemm_t<EPI_RESID_ADD_NORM, CG>(ta, tb, tc, td, a, stream);
     default: return fail(-2, "gemm: unknown epilogue %d", d.epilogue);
   }
 }
@@ -406,21 +526,32 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int cg = gemm_cta_group();
-  CUtensorMap ta, tb, tc;
+  CUtensorMap ta, tb, tc, td;
   if (!make_tmap_2d(&ta, d.A, 2, d.M, d.K, d.lda, GEMM_BM, GEMM_BK, true)) return -3;
   if (cached_b) tb = *cached_b;
   else if (!make_weight_tmap(&tb, d.B, d.N, d.K, d.ldb)) return -3;
   const int out_cols = d.epilogue == EPI_SWIGLU ? d.N / 2 : d.N;
-  if (d.epilogue == EPI_RESID_ADD) {
+  if (d.epilogue == EPI_RESID_ADD || d.epilogue == EPI_RESID_ADD_NORM) {
     if (!make_tmap_2d(&tc, d.C, 4, d.M, out_cols, d.ldc, 32, 32, true)) return -3;
   } else {
     if (!make_tmap_2d(&tc, d.C, 2, d.M, out_cols, d.ldc, 32, 64, true)) return -3;
+  }
+  if (d.epilogue == EPI_RESID_ADD_NORM) {
+    if (d.xb == nullptr || d.ss_out == nullptr) return fail(-2, "gemm: RESID_ADD_NORM needs xb and ss_out");
+    if (!make_tmap_2d(&td, d.xb, 2, d.M, out_cols, d.ldxb, 32, 64, true)) return -3;
+  } else {
+    td = tc;
   }
   GemmArgs a;
   a.M = d.M; a.N = d.N; a.K = d.K;
   a.num_n_blk = (d.N + GEMM_BN - 1) / GEMM_BN;
   a.pos = d.pos; a.rope_cos = d.rope_cos; a.rope_sin = d.rope_sin; a.rope_heads = d.rope_heads;
-  return cg == 2 ? dispatch_gemm<2>(d, ta, tb, tc, a, stream) : dispatch_gemm<1>(d, ta, tb, tc, a, stream);
+  a.row_ss = d.row_ss; a.ss_zero = d.ss_zero; a.ss_out = d.ss_out;
+  a.resid = reinterpret_cast<const float*>(d.C); a.ldr = d.ldc;
+  a.xb_out = d.xb; a.ldxb = d.ldxb;
+  a.inv_d = d.inv_d; a.eps = d.eps;
+  return cg == 2 ? dispatch_gemm<2>(d, ta, tb, tc, td, a, stream)
+                 : dispatch_gemm<1>(d, ta, tb, tc, td, a, stream);
 }
 
 }  // namespace pf

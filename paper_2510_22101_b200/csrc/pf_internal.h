@@ -12,6 +12,7 @@ enum Epilogue : int {
   EPI_ROPE_BF16 = 1,
   EPI_SWIGLU = 2,
   EPI_RESID_ADD = 3,
+  EPI_RESID_ADD_NORM = 4,   // resid += acc (fp32), xb = bf16(resid), ss_out[row] += sum(resid^2)
 };
 
 // ---- error state (thread-local message, negative return codes; see include/prefill_sm100.h)
@@ -39,16 +40,27 @@ struct GemmDesc {
   const float* rope_sin;
   int rope_heads;
   int max_seq;
+  // fused RMSNorm (see gemm.cu): A rows are bf16(residual); the epilogue multiplies row r by
+  // rsqrt(row_ss[r]/d + eps).  ss_zero rows are cleared by the n-tile-0 CTAs (for the next
+  // accumulation).  EPI_RESID_ADD_NORM also writes xb (bf16 copy) and accumulates ss_out.
+  const float* row_ss;
+  float* ss_zero;
+  float* ss_out;
+  void* xb;
+  int ldxb;
+  float inv_d, eps;
 };
 int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t stream);
 int gemm_smem_bytes();
 int gemm_cta_group();   // 2 (default) or 1 via PF_GEMM_CTAS=1
 bool make_weight_tmap(CUtensorMap* out, const void* B, int N, int K, int ldb);
 
-int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, int T, int d, int vocab,
-                 cudaStream_t stream);
+int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, void* xb, float* ss, int T,
+                 int d, cudaStream_t stream);
 int launch_rmsnorm(const float* resid, const float* gamma, void* out_bf16, int T, int d, float eps,
                    cudaStream_t stream);
+int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const float* resid,
+                       int d, void* attn_c, float* resid_c, cudaStream_t stream);
 int launch_head(const float* resid, const int32_t* last_idx, int n_items, int d,
                 const float* final_gamma, const float* w_yes, const float* w_no, float eps,
                 float* logits2, float* p_yes, int* bad_flag, cudaStream_t stream);

@@ -89,17 +89,14 @@ class PrefillScorer:
         self.device = torch.device(device)
         cfg = self.config
         w = weights
-        self._keep = [
-            _ptr_array(w.w_qkv), _ptr_array(w.w_o), _ptr_array(w.w_gu), _ptr_array(w.w_down),
-            _ptr_array(w.ln_attn), _ptr_array(w.ln_mlp),
-        ]
+        self._keep = [_ptr_array(w.w_qkv), _ptr_array(w.w_o), _ptr_array(w.w_gu), _ptr_array(w.w_down)]
         desc = _lib.PfModelDesc()
         desc.n_layers, desc.d_model = cfg.n_layers, cfg.d_model
         desc.n_heads, desc.n_kv_heads, desc.d_head = cfg.n_heads, cfg.n_kv_heads, cfg.d_head
         desc.d_ff, desc.d_ff_pad = cfg.d_ff, cfg.d_ff_pad
         desc.vocab_size, desc.max_seq, desc.rms_eps = cfg.vocab_size, cfg.max_seq, cfg.rms_eps
         desc.embedding = _ptr(w.embedding)
-        (desc.w_qkv, desc.w_o, desc.w_gu, desc.w_down, desc.ln_attn, desc.ln_mlp) = [
+        (desc.w_qkv, desc.w_o, desc.w_gu, desc.w_down) = [
             ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p)) for a in self._keep]
         desc.ln_final, desc.w_yes, desc.w_no = _ptr(w.ln_final), _ptr(w.w_yes), _ptr(w.w_no)
         desc.rope_cos, desc.rope_sin = _ptr(w.rope_cos), _ptr(w.rope_sin)

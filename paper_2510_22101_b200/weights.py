@@ -166,16 +166,23 @@ class DeviceWeights:
         return tot
 
 
-def _to_device_layer(cfg: ModelConfig, lw: dict, device):
+def _to_device_layer(cfg: ModelConfig, lw: dict, device, g_attn=None, g_mlp=None):
+    """RMSNorm is fused into the GEMM epilogues on the device, so the norm gains are folded into
+    the input rows of W_q/W_k/W_v and W_gate/W_up (fp32 product, then bf16).  Gains of 1.0 (the
+    pinned init) leave the weights bit-identical."""
     import torch
 
-    def dev(a):
+    def dev(a, g=None):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        if g is not None and not np.all(g == 1.0):
+            a = a * np.asarray(g, dtype=np.float32)[:, None]
         return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=torch.bfloat16)
 
-    wq, wk, wv = dev(lw["W_q"]), dev(lw["W_k"]), dev(lw["W_v"])
+    wq, wk, wv = dev(lw["W_q"], g_attn), dev(lw["W_k"], g_attn), dev(lw["W_v"], g_attn)
     w_qkv = torch.cat([wq, wk, wv], dim=1).t().contiguous()
     w_o = dev(lw["W_o"]).t().contiguous()
-    w_gu = interleave_gate_up(dev(lw["W_gate"]).t(), dev(lw["W_up"]).t(), cfg.d_ff_pad).contiguous()
+    w_gu = interleave_gate_up(dev(lw["W_gate"], g_mlp).t(), dev(lw["W_up"], g_mlp).t(),
+                              cfg.d_ff_pad).contiguous()
     wd = dev(lw["W_down"]).t()
     w_down = torch.zeros((cfg.d_model, cfg.d_ff_pad), dtype=torch.bfloat16, device=device)
     w_down[:, : cfg.d_ff] = wd
@@ -192,7 +199,7 @@ def to_device(weights: Weights, device="cuda") -> DeviceWeights:
     dw.embedding = torch.from_numpy(weights.token_embedding).to(device=device, dtype=torch.bfloat16)
     for lw in weights.layers:
         d = {f: getattr(lw, f) for f in LAYER_FIELDS}
-        a, b, c, e = _to_device_layer(cfg, d, device)
+        a, b, c, e = _to_device_layer(cfg, d, device, lw.rms_attn, lw.rms_mlp)
         dw.w_qkv.append(a); dw.w_o.append(b); dw.w_gu.append(c); dw.w_down.append(e)
         dw.ln_attn.append(torch.from_numpy(lw.rms_attn).to(device))
         dw.ln_mlp.append(torch.from_numpy(lw.rms_mlp).to(device))

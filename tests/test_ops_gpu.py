@@ -159,9 +159,13 @@ def test_embed_rmsnorm_head(lib):
     emb = rand_bf16(V, d, seed=12)
     ids = torch.randint(0, V, (T,), device="cuda", dtype=torch.int32)
     resid = torch.empty(T, d, device="cuda")
-    _lib.check(lib.pf_embed(P(ids), P(emb), P(resid), T, d, stream()))
+    xb = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    ss = torch.empty(T, device="cuda")
+    _lib.check(lib.pf_embed(P(ids), P(emb), P(resid), P(xb), P(ss), T, d, stream()))
     torch.cuda.synchronize()
     torch.testing.assert_close(resid, emb[ids.long()].float(), rtol=0, atol=0)
+    torch.testing.assert_close(xb, emb[ids.long()], rtol=0, atol=0)
+    torch.testing.assert_close(ss, emb[ids.long()].float().pow(2).sum(-1), rtol=1e-5, atol=1e-3)
 
     x = torch.randn(T, d, device="cuda") * 3
     g = torch.rand(d, device="cuda") + 0.5
@@ -188,3 +192,58 @@ def test_embed_rmsnorm_head(lib):
     torch.testing.assert_close(logits2[:, 1], ln, rtol=1e-4, atol=1e-4)
     torch.testing.assert_close(p, torch.sigmoid(ly - ln), rtol=1e-5, atol=1e-5)
     assert int(bad.item()) == 0
+
+
+def gemm_ex(lib, **kw):
+    a = _lib.PfGemmArgs()
+    for k, v in kw.items():
+        setattr(a, k, v.data_ptr() if hasattr(v, "data_ptr") else v)
+    _lib.check(lib.pf_gemm_bf16_ex(ctypes.byref(a), stream()))
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 256, 128), (5000, 2048, 1280)])
+def test_gemm_resid_add_norm(lib, M, N, K):
+    """Fused RMSNorm producer: C += A.B^T (fp32), xb = bf16(C), ss_out += row sum of squares."""
+    A = rand_bf16(M, K, seed=30)
+    B = rand_bf16(N, K, scale=K ** -0.5, seed=31)
+    C0 = torch.randn(M, N, device="cuda")
+    C = C0.clone()
+    xb = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    ss = torch.full((M,), 0.25, device="cuda")
+    gemm_ex(lib, A=A, lda=K, B=B, ldb=K, C=C, ldc=N, M=M, N=N, K=K, epilogue=_lib.EPI_RESID_ADD_NORM,
+            xb=xb, ldxb=N, ss_out=ss)
+    ref = C0 + A.float() @ B.float().t()
+    torch.testing.assert_close(C, ref, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(xb.float(), C.to(torch.bfloat16).float(), rtol=0, atol=0)
+    torch.testing.assert_close(ss, 0.25 + ref.pow(2).sum(-1), rtol=1e-4, atol=1e-2)
+
+
+def test_gemm_row_scaled_swiglu_and_rope(lib):
+    """Fused RMSNorm consumer: the accumulator row is scaled by rsqrt(ss/d + eps) before the
+    SwiGLU / RoPE epilogues; ss_zero rows are cleared."""
+    M, K, F = 900, 256, 384
+    x = torch.randn(M, K, device="cuda") * 3
+    xb = x.to(torch.bfloat16)
+    ss_in = xb.float().pow(2).sum(-1)
+    zero_me = torch.ones(M, device="cuda")
+    G = rand_bf16(F, K, scale=K ** -0.5, seed=32)
+    U = rand_bf16(F, K, scale=K ** -0.5, seed=33)
+    B = interleave_gate_up(G, U, F).contiguous()
+    C = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    gemm_ex(lib, A=xb, lda=K, B=B, ldb=K, C=C, ldc=F, M=M, N=2 * F, K=K, epilogue=_lib.EPI_SWIGLU,
+            row_ss=ss_in, ss_zero=zero_me, inv_d=1.0 / K, eps=1e-6)
+    xn = xb.float() * torch.rsqrt(ss_in / K + 1e-6)[:, None]
+    ref = torch.nn.functional.silu(xn @ G.float().t()) * (xn @ U.float().t())
+    torch.testing.assert_close(C.float(), ref, rtol=2e-2, atol=2e-2)
+    assert float(zero_me.abs().max()) == 0.0
+
+    cfg = ModelConfig(n_layers=1, d_model=K, n_heads=2, n_kv_heads=1, d_ff=128, d_head=128)
+    cos, sin = (torch.from_numpy(t).cuda() for t in rope_tables(cfg))
+    Bq = rand_bf16(512, K, scale=K ** -0.5, seed=34)
+    pos = torch.randint(0, 2048, (M,), device="cuda", dtype=torch.int32)
+    Cq = torch.empty(M, 512, device="cuda", dtype=torch.bfloat16)
+    gemm_ex(lib, A=xb, lda=K, B=Bq, ldb=K, C=Cq, ldc=512, M=M, N=512, K=K, epilogue=_lib.EPI_ROPE_BF16,
+            pos=pos, rope_cos=cos, rope_sin=sin, rope_heads=3, row_ss=ss_in, inv_d=1.0 / K, eps=1e-6)
+    refq = rope_ref(xn @ Bq.float().t(), pos, cos, sin, 3)
+    torch.testing.assert_close(Cq.float(), refq, rtol=1.6e-2, atol=2e-2)

@@ -138,6 +138,43 @@ def test_pruned_model_parity():
     assert np.max(np.abs(res.p_yes - p_ref)) <= TOL_P
 
 
+def test_last_layer_compaction_is_exact(monkeypatch):
+    """The last layer's O-projection + MLP run only on the last-token rows; per-row arithmetic is
+    unchanged, so scores are bit-identical to running them over every row."""
+    cfg = CONFIGS["TINY_GQA"]
+    w = init_weights(cfg, 0)
+    rng = np.random.default_rng(17)
+    packed = pack_requests([make_shared(rng, 64, list(rng.integers(1, 300, 20)), "spread"),
+                            make_shared(rng, 9, [5, 130], "template")])
+    compact = PrefillScorer(w).score_packed(packed)
+    monkeypatch.setenv("PF_NO_LAST_LAYER_COMPACT", "1")
+    full = PrefillScorer(w).score_packed(packed)
+    np.testing.assert_array_equal(compact.logits2, full.logits2)
+    np.testing.assert_array_equal(compact.p_yes, full.p_yes)
+
+
+def test_trained_norm_gains_parity():
+    """Non-unit RMSNorm gains (as a trained checkpoint has): the device folds them into W_qkv /
+    W_gate,up (RMSNorm fused into the GEMM epilogues); scores stay within tolerance."""
+    from paper_2510_22101_b200.weights import bf16_round
+
+    cfg = CONFIGS["TINY_GQA"]
+    w = init_weights(cfg, 0)
+    rng = np.random.default_rng(8)
+    for lw in w.layers:
+        lw.rms_attn = bf16_round(rng.uniform(0.5, 1.5, cfg.d_model).astype(np.float32))
+        lw.rms_mlp = bf16_round(rng.uniform(0.5, 1.5, cfg.d_model).astype(np.float32))
+    w.final_norm = bf16_round(rng.uniform(0.5, 1.5, cfg.d_model).astype(np.float32))
+    ow = OM.OracleWeights(cfg, w.token_embedding,
+                          [{**{f: getattr(lw, f) for f in OM.LAYER_FIELDS},
+                            "rms_attn": lw.rms_attn, "rms_mlp": lw.rms_mlp} for lw in w.layers],
+                          w.final_norm, w.head)
+    batches = [make_shared(rng, 64, list(rng.integers(1, 200, 24)), "spread")]
+    res = score_shared_batch(PrefillScorer(w), batches)
+    p_ref = oracle_scores(ow, batches)
+    assert np.max(np.abs(res.p_yes - p_ref)) <= TOL_P
+
+
 def test_graph_replay_matches_direct():
     from paper_2510_22101_b200.engine import DevicePacked
 

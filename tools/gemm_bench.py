@@ -21,6 +21,8 @@ SHAPES = [  # name, M, N (B rows), K, epilogue, useful flops (true widths)
     ("o+resid", T, 2048, 1280, _lib.EPI_RESID_ADD, 2 * T * 2048 * 1280),
     ("gate/up+swiglu", T, 7424, 2048, _lib.EPI_SWIGLU, 2 * T * 2048 * 2 * 3686),
     ("down+resid", T, 2048, 3712, _lib.EPI_RESID_ADD, 2 * T * 3686 * 2048),
+    ("o+resid+norm", T, 2048, 1280, _lib.EPI_RESID_ADD_NORM, 2 * T * 2048 * 1280),
+    ("down+resid+norm", T, 2048, 3712, _lib.EPI_RESID_ADD_NORM, 2 * T * 3686 * 2048),
     ("square bf16", 8192, 8192, 8192, _lib.EPI_BF16, 2 * 8192 ** 3),
 ]
 
@@ -54,10 +56,17 @@ def main():
         ncol = N // 2 if epi == _lib.EPI_SWIGLU else N
         C = torch.zeros(M, ncol, device="cuda", dtype=torch.float32 if epi == _lib.EPI_RESID_ADD else torch.bfloat16)
 
+        xb = torch.empty(M, ncol, device="cuda", dtype=torch.bfloat16) if epi == _lib.EPI_RESID_ADD_NORM else None
+        ss = torch.ones(M, device="cuda")
+        args = _lib.PfGemmArgs(A=A.data_ptr(), lda=K, B=B.data_ptr(), ldb=K, C=C.data_ptr(), ldc=ncol, M=M, N=N,
+                               K=K, epilogue=epi, pos=pos.data_ptr() if epi == 1 else None,
+                               rope_cos=cos.data_ptr(), rope_sin=sin.data_ptr(), rope_heads=15 if epi == 1 else 0,
+                               row_ss=ss.data_ptr() if epi in (1, 2) else None,
+                               ss_out=ss.data_ptr() if xb is not None else None,
+                               xb=xb.data_ptr() if xb is not None else None, ldxb=ncol, inv_d=1.0 / K, eps=1e-6)
+
         def ours():
-            _lib.check(lib.pf_gemm_bf16(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), ncol, M, N, K, epi,
-                                        pos.data_ptr() if epi == 1 else None, cos.data_ptr(), sin.data_ptr(),
-                                        (10 + 5) if epi == 1 else 0, stream))
+            _lib.check(lib.pf_gemm_bf16_ex(ctypes.byref(args), stream))
 
         Cb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         cublas = lambda: torch.matmul(A, B.t(), out=Cb)

@@ -5,7 +5,7 @@ import csv
 import re
 import sys
 
-EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add(O/down)"}
+EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add", "4": "resid-add+norm"}
 
 
 def main(path):

@@ -19,7 +19,7 @@ import bench  # noqa: E402
 from paper_2510_22101_b200 import CONFIGS, REQUESTS, init_device_weights  # noqa: E402
 from paper_2510_22101_b200.engine import DevicePacked, PrefillScorer  # noqa: E402
 
-EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add"}
+EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add", "4": "resid-add+norm"}
 
 
 def key(name):
