@@ -123,6 +123,10 @@ PF_API int pf_head_last_token(const float* resid, const int32_t* last_idx, int n
                        float eps, float* logits2, float* p_yes, int* bad_flag,
                        pf_stream_t stream);
 
+/* Debug hook: CTA 0 of the attention kernel appends {event, role, unit, block, globaltimer}
+ * records (uint64) to device_buf (NULL disables).  Used by tools/attn_trace.py. */
+PF_API int pf_debug_set_trace(void* device_buf, unsigned int capacity);
+
 PF_API const char* pf_last_error(void);
 PF_API const char* pf_version(void);
 

@@ -22,7 +22,7 @@ EPI_BF16, EPI_ROPE_BF16, EPI_SWIGLU, EPI_RESID_ADD, EPI_RESID_ADD_NORM = 0, 1, 2
 EXPORTED_SYMBOLS = (
     "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host",
     "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
-    "pf_last_error", "pf_version",
+    "pf_last_error", "pf_version", "pf_debug_set_trace",
 )
 
 
@@ -86,6 +86,7 @@ _SIGS = {
     "pf_rmsnorm": (_I, [_P, _P, _P, _I, _I, _F, _P]),
     "pf_prefix_attention": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _I, _P]),
     "pf_head_last_token": (_I, [_P, _P, _I, _I, _P, _P, _P, _F, _P, _P, _P, _P]),
+    "pf_debug_set_trace": (_I, [_P, ctypes.c_uint]),
     "pf_last_error": (ctypes.c_char_p, []),
     "pf_version": (ctypes.c_char_p, []),
 }

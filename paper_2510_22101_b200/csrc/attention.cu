@@ -13,12 +13,15 @@
 // query heads sharing g): both heads reuse every K/V block loaded.  64-key blocks (a 64-token
 // prefix is one block; a 100-token item two).  Warp roles (384 threads):
 //   WG0 / WG1   softmax for query head 0 / 1 of the pair: thread i owns row i (TMEM lane i);
-//               tcgen05.ld S -> mask -> exp2 -> bf16 P (swizzled smem).  O is accumulated by
-//               the tensor core in TMEM; the running max is only raised (and O rescaled in
-//               TMEM) when it grows by > 2^8 (lazy rescale), so most blocks never touch O.
-//   warp 8      TMA producer: Q pair per unit; K/V 64-key blocks through a 3-stage ring
-//   warp 9      TMEM owner + tcgen05.mma issuer: S_j = Q_j K^T (M128 N64 K128),
-//               O_j += P_j V (M128 N128 K64, V MN-major), ping-ponging the two heads
+//               tcgen05.ld S -> mask -> exp2 -> bf16 P written back to TMEM (tcgen05.st).
+//               O is accumulated by the tensor core in TMEM; the running max is only raised
+//               (and O rescaled in TMEM) when it grows by > 2^8 (lazy rescale).
+//   warp 8      TMA producer: Q pair per unit (double-buffered); K/V 64-key blocks, 3-stage ring
+//   warp 9      TMEM owner + tcgen05.mma issuer: S_j = Q_j K^T (SS, M128 N64 K128),
+//               O_j += P_j V (TS: P from TMEM, V MN-major from smem, M128 N128 K64)
+//   warps 10-11 fill a shared-memory table with this CTA's unit descriptors at kernel start
+// TMEM columns: S_0 [0,64) S_1 [64,128) O_0 [128,256) O_1 [256,384) P_0 [384,448) P_1 [448,512)
+// (P double-buffered: the issuer runs S(b+1) before PV(b) so softmax(b+1) overlaps PV(b)).
 #include <cuda_runtime.h>
 #include "ptx.cuh"
 #include "pf_internal.h"
@@ -31,16 +34,38 @@ constexpr int AT_STAGES = 3;
 constexpr int AT_QBOX = 128 * 64 * 2;           // [128 rows x 64 cols] bf16 = 16 KB
 constexpr int AT_KBOX = 64 * 64 * 2;            // [64 rows x 64 cols] bf16 = 8 KB
 constexpr int AT_Q_HEAD = 2 * AT_QBOX;          // one head's Q tile (dh = 128)
+constexpr int AT_Q_BUF = 2 * AT_Q_HEAD;         // a head pair
 constexpr int AT_KV_STAGE = 4 * AT_KBOX;        // K (2 boxes) + V (2 boxes)
-constexpr int AT_P_HEAD = 128 * 128;            // [128 rows x 64 keys] bf16
-constexpr int AT_OFF_KV = 2 * AT_Q_HEAD;
-constexpr int AT_OFF_P = AT_OFF_KV + AT_STAGES * AT_KV_STAGE;
-constexpr int AT_OFF_BAR = AT_OFF_P + 2 * AT_P_HEAD;
-constexpr int AT_SMEM = 1024 + AT_OFF_BAR + 256;
+constexpr int AT_OFF_KV = AT_Q_BUF;             // Q single-buffered
+constexpr int AT_OFF_OST = AT_OFF_KV + AT_STAGES * AT_KV_STAGE;   // O staging: [head][warp][2 x 4 KB]
+constexpr int AT_OST_WARP = 2 * 32 * 128;
+constexpr int AT_OFF_TAB = AT_OFF_OST + 8 * AT_OST_WARP;
+constexpr int AT_TAB = 32;                      // unit descriptors cached per CTA
+constexpr int AT_OFF_BAR = AT_OFF_TAB + AT_TAB * 48;
+constexpr int AT_SMEM = 1024 + AT_OFF_BAR + 160;
 constexpr float AT_RESCALE_THRESH = 8.0f;       // log2 units
+constexpr uint32_t AT_TS = 0, AT_TO = 128, AT_TP = 384;   // TMEM column bases (P: [head][2 bufs] x 32)
+
+// ---- debug trace (pf_debug_set_trace): CTA 0 appends {event, unit, block, ns} records
+__device__ unsigned long long* g_att_trace = nullptr;
+__device__ unsigned int g_att_trace_n = 0;
+__device__ unsigned int g_att_trace_cap = 0;
+enum AttEvt { EV_QFULL = 1, EV_KVFULL, EV_S_ISSUED, EV_PREADY, EV_PV_ISSUED, EV_SFULL, EV_PARRIVE, EV_ODONE, EV_EPI_DONE,
+              EV_UNIT_START, EV_END };
+PF_DEVICE void att_trace(int ev, int unit, int blk, int who) {
+  // atomic-free: fixed slot per (role, unit, block, event) so tracing adds no round trips
+  if (g_att_trace == nullptr || blockIdx.x != 0 || (threadIdx.x & 31) != 0) return;
+  const int role = who == 8 ? 0 : (who == 9 || who == 25) ? 1 : 2 + (who & 1);
+  if (unit >= 64 || blk >= 8) return;
+  const unsigned int i = ((role * 64 + unit) * 8 + blk) * 16 + ev + (who == 25 ? 11 : 0);
+  if (i >= g_att_trace_cap) return;
+  g_att_trace[i] = ((unsigned long long)ev << 56) | ((unsigned long long)(who & 0xff) << 48) |
+                   ((unsigned long long)(unit & 0xff) << 40) | ((unsigned long long)(blk & 0xff) << 32) |
+                   (globaltimer_ns() & 0xffffffffull);
+}
 
 struct UnitInfo {
-  int q_row0, q_len, q_local0, kv_off, kv_len, q_off, n_pre, n_blk, h0, nh, g;
+  int q_row0, q_len, q_local0, kv_off, kv_len, q_off, n_pre, n_blk, h0, nh, g, pad;
 };
 
 PF_DEVICE UnitInfo decode_unit(const AttnDesc& d, int u, int r, int n_pairs) {
@@ -61,26 +86,28 @@ PF_DEVICE UnitInfo decode_unit(const AttnDesc& d, int u, int r, int n_pairs) {
   ui.n_blk = ui.n_pre + (q_end + AT_KB - 1) / AT_KB;
   ui.h0 = ui.g * r + 2 * p;
   ui.nh = min(2, r - 2 * p);
+  ui.pad = 0;
   return ui;
 }
 
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_prefix_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
-                       const AttnDesc d, int n_units) {
+                       const __grid_constant__ CUtensorMap tmO, const AttnDesc d, int n_units) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + AT_OFF_KV;
-  uint8_t* sP = smem + AT_OFF_P;
+  UnitInfo* tab = reinterpret_cast<UnitInfo*>(smem + AT_OFF_TAB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AT_OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;            // [3]
-  uint64_t* kv_empty = bars + 5;           // [3]
-  uint64_t* s_full = bars + 8;             // [2]
-  uint64_t* p_ready = bars + 10;           // [2]
-  uint64_t* o_done = bars + 12;            // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* q_full = bars + 0;             // [2]
+  uint64_t* q_empty = bars + 2;            // [2]
+  uint64_t* kv_full = bars + 4;            // [3]
+  uint64_t* kv_empty = bars + 7;           // [3]
+  uint64_t* s_full = bars + 10;            // [2]
+  uint64_t* p_ready = bars + 12;           // [2]
+  uint64_t* o_done = bars + 14;            // [2]
+  uint64_t* pv_done = bars + 16;           // [2]  one phase per PV_j
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -90,130 +117,182 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmKV);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    tma_prefetch_desc(&tmO);
+    for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
     for (int s = 0; s < AT_STAGES; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int j = 0; j < 2; ++j) { mbar_init(&s_full[j], 1); mbar_init(&p_ready[j], 4); mbar_init(&o_done[j], 1); }
+    for (int j = 0; j < 2; ++j) { mbar_init(&s_full[j], 1); mbar_init(&p_ready[j], 4); mbar_init(&o_done[j], 1); mbar_init(&pv_done[j], 1); }
     fence_barrier_init();
+  }
+  if (warp >= 10) {   // unit-descriptor table: one global round trip per CTA instead of per unit
+    for (int i = threadIdx.x - 320; i < AT_TAB; i += 64) {
+      const int u = blockIdx.x + i * gridDim.x;
+      if (u < n_units) tab[i] = decode_unit(d, u, r, n_pairs);
+    }
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  auto unit = [&](int u, int k) { return k < AT_TAB ? tab[k] : decode_unit(d, u, r, n_pairs); };
 
   if (warp == 8) {
-    if (lane == 0) {
-      // ------------------------------------------------------------------ TMA producer
-      uint32_t kv_it = 0, q_it = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const UnitInfo ui = decode_unit(d, u, r, n_pairs);
-        mbar_wait(q_empty, (q_it & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, ui.nh * AT_Q_HEAD);
+    // ---------------------------------------------------------------------- TMA producer
+    uint32_t kv_it = 0, q_it = 0;
+    int k = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++k) {
+      const UnitInfo ui = unit(u, k);
+      const int qb = 0;
+      att_trace(EV_UNIT_START, k, ui.n_blk, 8);
+      mbar_wait(&q_empty[qb], (q_it & 1) ^ 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&q_full[qb], ui.nh * AT_Q_HEAD);
         for (int j = 0; j < ui.nh; ++j) {
           const int qc = (ui.h0 + j) * d.dh;
-          tma_load_2d(sQ + j * AT_Q_HEAD, &tmQ, q_full, qc, ui.q_row0, kEvictFirst);
-          tma_load_2d(sQ + j * AT_Q_HEAD + AT_QBOX, &tmQ, q_full, qc + 64, ui.q_row0, kEvictFirst);
+          uint8_t* dst = sQ + qb * AT_Q_BUF + j * AT_Q_HEAD;
+          tma_load_2d(dst, &tmQ, &q_full[qb], qc, ui.q_row0, kEvictFirst);
+          tma_load_2d(dst + AT_QBOX, &tmQ, &q_full[qb], qc + 64, ui.q_row0, kEvictFirst);
         }
-        ++q_it;
-        const int kc = (d.H + ui.g) * d.dh;
-        const int vc = (d.H + d.Hkv + ui.g) * d.dh;
-        for (int b = 0; b < ui.n_blk; ++b, ++kv_it) {
-          const int st = kv_it % AT_STAGES;
-          mbar_wait(&kv_empty[st], ((kv_it / AT_STAGES) & 1) ^ 1);
-          const int krow = b < ui.n_pre ? ui.kv_off + b * AT_KB : ui.q_off + (b - ui.n_pre) * AT_KB;
-          uint8_t* dst = sKV + st * AT_KV_STAGE;
+      }
+      __syncwarp();
+      ++q_it;
+      const int kc = (d.H + ui.g) * d.dh;
+      const int vc = (d.H + d.Hkv + ui.g) * d.dh;
+      for (int b = 0; b < ui.n_blk; ++b, ++kv_it) {
+        const int st = kv_it % AT_STAGES;
+        mbar_wait(&kv_empty[st], ((kv_it / AT_STAGES) & 1) ^ 1);
+        const int krow = b < ui.n_pre ? ui.kv_off + b * AT_KB : ui.q_off + (b - ui.n_pre) * AT_KB;
+        uint8_t* dst = sKV + st * AT_KV_STAGE;
+        if (elect_one()) {
           mbar_arrive_expect_tx(&kv_full[st], AT_KV_STAGE);
           tma_load_2d(dst, &tmKV, &kv_full[st], kc, krow, kEvictLast);
           tma_load_2d(dst + AT_KBOX, &tmKV, &kv_full[st], kc + 64, krow, kEvictLast);
           tma_load_2d(dst + 2 * AT_KBOX, &tmKV, &kv_full[st], vc, krow, kEvictLast);
           tma_load_2d(dst + 3 * AT_KBOX, &tmKV, &kv_full[st], vc + 64, krow, kEvictLast);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      // ------------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, AT_KB, false, false);
-      constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);   // V is MN-major
-      uint32_t kv_it = 0, q_it = 0;
-      uint32_t blk_it[2] = {0, 0};
-      const uint32_t q_addr = smem_u32(sQ);
-      const uint32_t p_addr = smem_u32(sP);
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const UnitInfo ui = decode_unit(d, u, r, n_pairs);
-        mbar_wait(q_full, q_it & 1);
-        tc_fence_after();
-        for (int b = 0; b < ui.n_blk; ++b, ++kv_it) {
-          const int st = kv_it % AT_STAGES;
-          mbar_wait(&kv_full[st], (kv_it / AT_STAGES) & 1);
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(sKV + st * AT_KV_STAGE);
-          const uint32_t v_addr = k_addr + 2 * AT_KBOX;
-          for (int j = 0; j < ui.nh; ++j) {
+    // ---------------------------------------------------------------------- MMA issuer
+    // Warp-converged loop (uniform descriptors in uniform registers); one elected lane issues.
+    // Software-pipelined: once softmax_j has consumed S_j(b) (p_ready), S_j(b+1) is issued ahead
+    // of PV_j(b), so the tensor core computes the next scores while softmax_j waits for nothing.
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, AT_KB, false, false);
+    constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);   // V is MN-major
+    uint32_t kv_it = 0, q_it = 0, blk0 = 0, blk1 = 0;
+    const uint64_t q_desc = kmajor_desc(smem_u32(sQ));
+    int k = 0;
+    auto issue_s = [&](int j, uint32_t st) {
+      const uint64_t k_desc = kmajor_desc(smem_u32(sKV + st * AT_KV_STAGE));
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              umma_bf16_ss(tmem_base + j * AT_KB,
-                           kmajor_desc(q_addr + j * AT_Q_HEAD + (k >> 2) * AT_QBOX + (k & 3) * 32),
-                           kmajor_desc(k_addr + (k >> 2) * AT_KBOX + (k & 3) * 32), idesc_s, k != 0);
-            }
-            umma_commit(&s_full[j]);
-          }
-          if (b == ui.n_blk - 1) umma_commit(q_empty);
-          for (int j = 0; j < ui.nh; ++j) {
-            mbar_wait(&p_ready[j], blk_it[j] & 1);
-            ++blk_it[j];
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < AT_KB / 16; ++k) {
-              umma_bf16_ss(tmem_base + 128 + j * 128, kmajor_desc(p_addr + j * AT_P_HEAD + k * 32),
-                           sw128_desc(v_addr + k * 2048, AT_KBOX, 1024), idesc_o, (b | k) != 0);
-            }
-            if (b == ui.n_blk - 1) umma_commit(&o_done[j]);
-          }
-          umma_commit(&kv_empty[st]);
-        }
-        ++q_it;
+      for (int kk = 0; kk < 8; ++kk) {   // descriptor start field is in 16-byte units
+        const uint32_t qo = (j * AT_Q_HEAD + (kk >> 2) * AT_QBOX + (kk & 3) * 32) >> 4;
+        const uint32_t ko = ((kk >> 2) * AT_KBOX + (kk & 3) * 32) >> 4;
+        umma_bf16_ss(tmem_base + AT_TS + j * AT_KB, q_desc + qo, k_desc + ko, idesc_s, kk != 0);
       }
+      umma_commit(&s_full[j]);
+    };
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++k) {
+      const UnitInfo ui = unit(u, k);
+      mbar_wait(&q_full[0], q_it & 1);
+      att_trace(EV_QFULL, k, 0, 9);
+      // prologue: S(0) for both heads
+      uint32_t st = kv_it % AT_STAGES;
+      mbar_wait(&kv_full[st], (kv_it / AT_STAGES) & 1);
+      att_trace(EV_KVFULL, k, 0, 9);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int j = 0; j < ui.nh; ++j) issue_s(j, st);
+        if (ui.n_blk == 1) umma_commit(&q_empty[0]);
+      }
+      __syncwarp();
+      for (int b = 0; b < ui.n_blk; ++b) {
+        const uint32_t st_b = (kv_it + b) % AT_STAGES;
+        const bool more = b + 1 < ui.n_blk;
+        const uint32_t st_n = (kv_it + b + 1) % AT_STAGES;
+        if (more) {
+          mbar_wait(&kv_full[st_n], ((kv_it + b + 1) / AT_STAGES) & 1);
+          att_trace(EV_KVFULL, k, b + 1, 9);
+        }
+        const uint32_t v_addr = smem_u32(sKV + st_b * AT_KV_STAGE) + 2 * AT_KBOX;
+        for (int j = 0; j < ui.nh; ++j) {
+          uint32_t& bi = j == 0 ? blk0 : blk1;
+          const uint32_t pbuf = bi & 1;
+          mbar_wait(&p_ready[j], bi & 1);
+          ++bi;
+          att_trace(EV_PREADY, k, b, 9 + 16 * j);
+          tc_fence_after();
+          if (elect_one()) {
+            if (more) {
+              issue_s(j, st_n);
+              if (b + 1 == ui.n_blk - 1 && j == ui.nh - 1) umma_commit(&q_empty[0]);
+            }
+#pragma unroll
+            for (int kk = 0; kk < AT_KB / 16; ++kk) {
+              umma_bf16_ts(tmem_base + AT_TO + j * 128, tmem_base + AT_TP + j * 64 + pbuf * 32 + kk * 8,
+                           sw128_desc(v_addr + kk * 2048, AT_KBOX, 1024), idesc_o, (b | kk) != 0);
+            }
+            umma_commit(&pv_done[j]);
+            if (!more) umma_commit(&o_done[j]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) umma_commit(&kv_empty[st_b]);
+        __syncwarp();
+      }
+      kv_it += ui.n_blk;
+      ++q_it;
     }
   } else if (warp < 8) {
     // -------------------------------------------------------------------- softmax WG j
     const int j = warp >> 2;
     const uint32_t row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem_base + lane_base + j * AT_KB;
-    const uint32_t tO = tmem_base + lane_base + 128 + j * 128;
-    const uint32_t p_row = smem_u32(sP + j * AT_P_HEAD) + row * 128;
+    const uint32_t tS = tmem_base + lane_base + AT_TS + j * AT_KB;
+    const uint32_t tO = tmem_base + lane_base + AT_TO + j * 128;
+    const uint32_t tP = tmem_base + lane_base + AT_TP + j * 64;
     const float sl2 = d.scale * 1.4426950408889634f;
     uint32_t blk_it = 0, u_it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const UnitInfo ui = decode_unit(d, u, r, n_pairs);
+    int k = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++k) {
+      const UnitInfo ui = unit(u, k);
       if (j >= ui.nh) continue;
       const int q_local = ui.q_local0 + (int)row;
-      float m_used = -INFINITY, l_run = 0.f;
+      float m_used = -INFINITY, l_run = 0.f;   // m_used in scaled (log2) units
       for (int b = 0; b < ui.n_blk; ++b, ++blk_it) {
         const bool is_pre = b < ui.n_pre;
         const int lim = is_pre ? (ui.kv_len - b * AT_KB) : (q_local - (b - ui.n_pre) * AT_KB + 1);
+        const bool full = __all_sync(0xffffffffu, lim >= AT_KB);
         mbar_wait(&s_full[j], blk_it & 1);
+        if (lane == 0 && (warp & 3) == 0) att_trace(EV_SFULL, k, b, j);
         tc_fence_after();
         uint32_t s[2][32];
         tmem_ld_32x32b_x32(tS, s[0]);
         tmem_ld_32x32b_x32(tS + 32, s[1]);
         tmem_ld_wait();
-        float mx = -INFINITY;
+        if (!full) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = (c * 32 + i < lim) ? __uint_as_float(s[c][i]) * sl2 : -INFINITY;
-            s[c][i] = __float_as_uint(x);
-            mx = fmaxf(mx, x);
-          }
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i >= lim) s[c][i] = __float_as_uint(-INFINITY);
+        }
+        float mxv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mxv[i] = __uint_as_float(s[0][i]);
+#pragma unroll
+        for (int i = 8; i < 64; ++i) mxv[i & 7] = fmaxf(mxv[i & 7], __uint_as_float(s[i >> 5][i & 31]));
+        const float mx = sl2 * fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
+                                     fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
         const bool need = mx > m_used + AT_RESCALE_THRESH;
-        bool rescaled = false;
         if (__any_sync(0xffffffffu, need)) {
           const float m_new = fmaxf(m_used, mx);
           if (b > 0) {
+            // PV of the previous block may still be accumulating into O: wait for it.  (The
+            // parity is unambiguous: PV(blk_it-2) completed before S(blk_it) was issued.)
+            mbar_wait(&pv_done[j], (blk_it - 1) & 1);
+            tc_fence_after();
             const float alpha = exp2f(m_used - m_new);
             l_run *= alpha;
 #pragma unroll 1
@@ -225,41 +304,44 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
               for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
               tmem_st_32x32b_x32(tO + c * 32, o);
             }
-            rescaled = true;
           }
           m_used = m_new;
         }
-        float sum = 0.f;
+        float sumv[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t w[32];
+        const float neg_m = -m_used;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t w[16];
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float p0 = exp2f(__uint_as_float(s[c][2 * i]) - m_used);
-            const float p1 = exp2f(__uint_as_float(s[c][2 * i + 1]) - m_used);
-            sum += p0 + p1;
-            w[i] = pack_bf16x2(p0, p1);
+            const float p0 = exp2f(fmaf(__uint_as_float(s[c][2 * i]), sl2, neg_m));
+            const float p1 = exp2f(fmaf(__uint_as_float(s[c][2 * i + 1]), sl2, neg_m));
+            sumv[i & 3] += p0 + p1;                // 4 independent chains
+            w[c * 16 + i] = pack_bf16x2(p0, p1);   // TMEM A operand: 2 keys per 32-bit column
           }
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const uint32_t chunk = c * 4 + q4;
-            st_shared_v4(p_row + ((chunk ^ (row & 7)) << 4), w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2],
-                         w[4 * q4 + 3]);
-          }
-        }
-        l_run += sum;
-        if (rescaled) tmem_st_wait();
-        fence_proxy_async_smem();
+        tmem_st_32x32b_x32(tP + (blk_it & 1) * 32, w);
+        l_run += (sumv[0] + sumv[1]) + (sumv[2] + sumv[3]);
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_ready[j]);
+        if (lane == 0 && (warp & 3) == 0) att_trace(EV_PARRIVE, k, b, j);
       }
       // ---- unit epilogue: O / l -> bf16 -> global
       mbar_wait(&o_done[j], u_it & 1);
+      if (lane == 0 && (warp & 3) == 0) att_trace(EV_ODONE, k, 0, j);
       ++u_it;
       tc_fence_after();
       const float inv = 1.f / l_run;
       const bool valid = q_local < ui.q_len;
+      // rows of this warp: [q_row0 + 32*(warp&3), +32); TMA-store them when all 32 belong to the
+      // segment, else write the valid rows directly (never touch the next segment's rows)
+      const bool warp_full = ui.q_local0 + (int)(warp & 3) * 32 + 31 < ui.q_len;
+      uint8_t* ost = smem + AT_OFF_OST + (j * 4 + (warp & 3)) * AT_OST_WARP;
+      if (warp_full) {
+        if (lane == 0) tma_store_wait_read<0>();   // previous unit's store has left the buffer
+        __syncwarp();
+      }
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(d.out) +
                                             (size_t)(ui.q_row0 + row) * (d.H * d.dh) + (ui.h0 + j) * d.dh);
 #pragma unroll 1
@@ -267,28 +349,55 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         uint32_t o[32];
         tmem_ld_32x32b_x32(tO + c * 32, o);
         tmem_ld_wait();
-        if (valid) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 v;
-            v.x = pack_bf16x2(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-            v.y = pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-            v.z = pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-            v.w = pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+        for (int q = 0; q < 4; ++q) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+          v.y = pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+          v.z = pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+          v.w = pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+          if (warp_full) {
+            // 64-column SW128 box (c >> 1); 16 B chunk (c & 1) * 4 + q of this row
+            const uint32_t chunk = (c & 1) * 4 + q;
+            st_shared_v4(smem_u32(ost + (c >> 1) * 4096) + lane * 128 + ((chunk ^ (lane & 7)) << 4), v.x, v.y,
+                         v.z, v.w);
+          } else if (valid) {
             dst[c * 4 + q] = v;
           }
         }
       }
+      if (warp_full) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int r0 = ui.q_row0 + (warp & 3) * 32;
+          const int c0 = (ui.h0 + j) * d.dh;
+          tma_store_2d(&tmO, ost, c0, r0);
+          tma_store_2d(&tmO, ost + 4096, c0 + 64, r0);
+          tma_store_commit();
+        }
+      }
+      if (lane == 0 && (warp & 3) == 0) att_trace(EV_EPI_DONE, k, 0, j);
       tc_fence_before();
     }
   }
 
+  if (warp < 8 && lane == 0) tma_store_wait_all<0>();
   tc_fence_before();
   __syncthreads();
   if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
   }
+}
+
+int debug_set_attention_trace(unsigned long long* buf, unsigned int cap) {
+  unsigned int zero = 0;
+  cudaMemcpyToSymbol(g_att_trace, &buf, sizeof(buf));
+  cudaMemcpyToSymbol(g_att_trace_n, &zero, sizeof(zero));
+  cudaMemcpyToSymbol(g_att_trace_cap, &cap, sizeof(cap));
+  cudaError_t e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? 0 : fail(-4, "trace setup: %s", cudaGetErrorString(e));
 }
 
 static int g_att_sms = 0;
@@ -301,6 +410,9 @@ int launch_attention(const AttnDesc& d, cudaStream_t stream) {
   CUtensorMap tq, tkv;
   if (!make_tmap_2d(&tq, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, 128, 64, true)) return -3;
   if (!make_tmap_2d(&tkv, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, AT_KB, 64, true)) return -3;
+  CUtensorMap to;
+  const int ldo = d.H * d.dh;
+  if (!make_tmap_2d(&to, d.out, 2, (uint64_t)d.T, (uint64_t)ldo, (uint64_t)ldo, 32, 64, true)) return -3;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
@@ -312,7 +424,7 @@ int launch_attention(const AttnDesc& d, cudaStream_t stream) {
   const int r = d.H / d.Hkv;
   const int n_units = d.n_work * d.Hkv * ((r + 1) / 2);
   const int grid = n_units < g_att_sms ? n_units : g_att_sms;
-  attn_prefix_kernel<<<grid, AT_THREADS, AT_SMEM, stream>>>(tq, tkv, d, n_units);
+  attn_prefix_kernel<<<grid, AT_THREADS, AT_SMEM, stream>>>(tq, tkv, to, d, n_units);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(-4, "attention launch: %s", cudaGetErrorString(e));
   return 0;

@@ -133,6 +133,10 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
 extern "C" {
 
 const char* pf_last_error(void) { return g_err; }
+int pf_debug_set_trace(void* device_buf, unsigned int capacity) {
+  return debug_set_attention_trace(reinterpret_cast<unsigned long long*>(device_buf), capacity);
+}
+
 const char* pf_version(void) { return "prefill_sm100 0.1 (tcgen05 bf16, sm_100a)"; }
 
 int pf_model_create(const pf_model_desc* desc, pf_model** out) {

@@ -138,15 +138,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer (each CTA)
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = grp; tile < num_tiles; tile += ngrp) {
-        const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
-        const int n0 = (tile % args.num_n_blk) * GEMM_BN + rank * Cfg::B_ROWS;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+    // -------------------------------------------------------------- TMA producer (each CTA)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = grp; tile < num_tiles; tile += ngrp) {
+      const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
+      const int n0 = (tile % args.num_n_blk) * GEMM_BN + rank * Cfg::B_ROWS;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (elect_one()) {
           if constexpr (CG == 2) {
             // both CTAs' bytes complete on the leader's barrier; only the leader arms it
             const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
@@ -158,18 +158,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tma_load_2d(sA + stage * GEMM_A_BYTES, &tmA, &full_bar[stage], kb * GEMM_BK, m0);
             tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full_bar[stage], kb * GEMM_BK, n0, kEvictLast);
           }
-          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {
       // ------------------------------------------------------------ MMA issuer (leader CTA)
+      // The whole warp runs the loop (warp-uniform control flow and descriptors, so they live in
+      // uniform registers); one elected lane issues the tcgen05 instructions.
       constexpr uint32_t idesc = make_idesc_bf16(Cfg::TILE_M, GEMM_BN, false, false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
       for (int tile = grp; tile < num_tiles; tile += ngrp) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -177,23 +181,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * GEMM_A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint64_t a_desc = kmajor_desc(a_base + stage * GEMM_A_BYTES);
+          const uint64_t b_desc = kmajor_desc(b_base + stage * Cfg::B_BYTES);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            if constexpr (CG == 2)
-              umma_bf16_ss_pair(d_tmem, kmajor_desc(a_addr + k * 32), kmajor_desc(b_addr + k * 32), idesc,
-                                (kb | k) != 0 ? 1u : 0u);
-            else
-              umma_bf16_ss(d_tmem, kmajor_desc(a_addr + k * 32), kmajor_desc(b_addr + k * 32), idesc,
-                           (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              // +32 B along K inside the 128 B swizzle row = +2 in the descriptor's start field
+              if constexpr (CG == 2)
+                umma_bf16_ss_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+              else
+                umma_bf16_ss(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            if constexpr (CG == 2) umma_commit_pair(&empty_bar[stage], 0x3);
+            else umma_commit(&empty_bar[stage]);
           }
-          if constexpr (CG == 2) umma_commit_pair(&empty_bar[stage], 0x3);
-          else umma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
-        if constexpr (CG == 2) umma_commit_pair(&tfull_bar[acc], 0x3);
-        else umma_commit(&tfull_bar[acc]);
+        if (elect_one()) {
+          if constexpr (CG == 2) umma_commit_pair(&tfull_bar[acc], 0x3);
+          else umma_commit(&tfull_bar[acc]);
+        }
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }

@@ -75,5 +75,6 @@ struct AttnDesc {
   float scale;
 };
 int launch_attention(const AttnDesc& d, cudaStream_t stream);
+int debug_set_attention_trace(unsigned long long* buf, unsigned int cap);
 
 }  // namespace pf
