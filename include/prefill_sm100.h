@@ -45,6 +45,7 @@ typedef struct pf_model pf_model;        /* opaque: config + cached weight TMA d
  *   ln_final : fp32 [d_model] final RMSNorm scale (applied in the head kernel)
  *   w_yes, w_no: fp32 [d_model] — columns yes_id / no_id of the [d_model x vocab] output head
  *   rope_cos, rope_sin: fp32 [max_seq x d_head/2]  (theta^(-2i/d_head) * pos, rotate-half)
+ *   d_head: 64 or 128.
  */
 typedef struct pf_model_desc {
   int n_layers, d_model, n_heads, n_kv_heads, d_head, d_ff, d_ff_pad, vocab_size, max_seq;
@@ -95,7 +96,8 @@ PF_API int pf_score_host(pf_model* model, const int32_t* ids, const int32_t* pos
                   float* p_yes_host, pf_stream_t stream);
 
 /* Per-op entry points (unit parity tests). */
-/* C = A[MxK] . B[NxK]^T with epilogue 0 bf16, 1 bf16+RoPE, 2 SwiGLU(bf16, N/2 cols),
+/* C = A[MxK] . B[NxK]^T (RoPE heads 128 wide here; pf_gemm_bf16_ex takes rope_dh 64/128)
+ * with epilogue 0 bf16, 1 bf16+RoPE, 2 SwiGLU(bf16, N/2 cols),
  * 3 fp32 C += (residual add), 4 fp32 C += acc with xb = bf16(C) and ss_out[row] += sum(C^2). */
 PF_API int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
                  int K, int epilogue, const int32_t* pos, const float* rope_cos,
@@ -105,7 +107,7 @@ PF_API int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C,
 typedef struct pf_gemm_args {
   const void* A; int lda; const void* B; int ldb; void* C; int ldc;
   int M, N, K, epilogue;
-  const int32_t* pos; const float* rope_cos; const float* rope_sin; int rope_heads;
+  const int32_t* pos; const float* rope_cos; const float* rope_sin; int rope_heads; int rope_dh;
   const float* row_ss; float* ss_zero; float* ss_out; void* xb; int ldxb; float inv_d, eps;
 } pf_gemm_args;
 PF_API int pf_gemm_bf16_ex(const pf_gemm_args* args, pf_stream_t stream);

@@ -63,7 +63,7 @@ class PfGemmArgs(ctypes.Structure):
         ("C", ctypes.c_void_p), ("ldc", ctypes.c_int),
         ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int), ("epilogue", ctypes.c_int),
         ("pos", ctypes.c_void_p), ("rope_cos", ctypes.c_void_p), ("rope_sin", ctypes.c_void_p),
-        ("rope_heads", ctypes.c_int),
+        ("rope_heads", ctypes.c_int), ("rope_dh", ctypes.c_int),
         ("row_ss", ctypes.c_void_p), ("ss_zero", ctypes.c_void_p), ("ss_out", ctypes.c_void_p),
         ("xb", ctypes.c_void_p), ("ldxb", ctypes.c_int), ("inv_d", ctypes.c_float), ("eps", ctypes.c_float),
     ]

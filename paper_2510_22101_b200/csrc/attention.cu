@@ -33,18 +33,25 @@ constexpr int AT_KB = 64;                       // keys per block
 constexpr int AT_STAGES = 3;
 constexpr int AT_QBOX = 128 * 64 * 2;           // [128 rows x 64 cols] bf16 = 16 KB
 constexpr int AT_KBOX = 64 * 64 * 2;            // [64 rows x 64 cols] bf16 = 8 KB
-constexpr int AT_Q_HEAD = 2 * AT_QBOX;          // one head's Q tile (dh = 128)
-constexpr int AT_Q_BUF = 2 * AT_Q_HEAD;         // a head pair
-constexpr int AT_KV_STAGE = 4 * AT_KBOX;        // K (2 boxes) + V (2 boxes)
-constexpr int AT_OFF_KV = AT_Q_BUF;             // Q single-buffered
-constexpr int AT_OFF_OST = AT_OFF_KV + AT_STAGES * AT_KV_STAGE;   // O staging: [head][warp][2 x 4 KB]
-constexpr int AT_OST_WARP = 2 * 32 * 128;
-constexpr int AT_OFF_TAB = AT_OFF_OST + 8 * AT_OST_WARP;
 constexpr int AT_TAB = 32;                      // unit descriptors cached per CTA
-constexpr int AT_OFF_BAR = AT_OFF_TAB + AT_TAB * 48;
-constexpr int AT_SMEM = 1024 + AT_OFF_BAR + 160;
 constexpr float AT_RESCALE_THRESH = 8.0f;       // log2 units
-constexpr uint32_t AT_TS = 0, AT_TO = 128, AT_TP = 384;   // TMEM column bases (P: [head][2 bufs] x 32)
+
+// Layout for head width DH (64 or 128): tiles are built from 64-column SW128 boxes.
+template <int DH>
+struct AtCfg {
+  static constexpr int NBX = DH / 64;                           // boxes per head row
+  static constexpr int Q_HEAD = NBX * AT_QBOX;                  // one head's 128-row Q tile
+  static constexpr int Q_BUF = 2 * Q_HEAD;                      // a head pair (single-buffered)
+  static constexpr int KV_STAGE = 2 * NBX * AT_KBOX;            // K boxes then V boxes
+  static constexpr int OFF_KV = Q_BUF;
+  static constexpr int OFF_OST = OFF_KV + AT_STAGES * KV_STAGE; // O staging [head][warp][NBX x 4 KB]
+  static constexpr int OST_WARP = NBX * 32 * 128;
+  static constexpr int OFF_TAB = OFF_OST + 8 * OST_WARP;
+  static constexpr int OFF_BAR = OFF_TAB + AT_TAB * 48;
+  static constexpr int SMEM = 1024 + OFF_BAR + 160;
+  // TMEM columns: S_j at 64 j, O_j at 128 + DH j, P_j[buf] at 128 + 2 DH + 64 j + 32 buf
+  static constexpr uint32_t TS = 0, TO = 128, TP = 128 + 2 * DH;
+};
 
 // ---- debug trace (pf_debug_set_trace): CTA 0 appends {event, unit, block, ns} records
 __device__ unsigned long long* g_att_trace = nullptr;
@@ -90,9 +97,16 @@ PF_DEVICE UnitInfo decode_unit(const AttnDesc& d, int u, int r, int n_pairs) {
   return ui;
 }
 
+template <int DH>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attn_prefix_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                        const __grid_constant__ CUtensorMap tmO, const AttnDesc d, int n_units) {
+  using C = AtCfg<DH>;
+  constexpr int AT_Q_HEAD = C::Q_HEAD, AT_Q_BUF = C::Q_BUF, AT_KV_STAGE = C::KV_STAGE;
+  constexpr int AT_OFF_KV = C::OFF_KV, AT_OFF_OST = C::OFF_OST, AT_OST_WARP = C::OST_WARP;
+  constexpr int AT_OFF_TAB = C::OFF_TAB, AT_OFF_BAR = C::OFF_BAR;
+  constexpr uint32_t AT_TS = C::TS, AT_TO = C::TO, AT_TP = C::TP;
+  constexpr int NBX = C::NBX;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -150,8 +164,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int j = 0; j < ui.nh; ++j) {
           const int qc = (ui.h0 + j) * d.dh;
           uint8_t* dst = sQ + qb * AT_Q_BUF + j * AT_Q_HEAD;
-          tma_load_2d(dst, &tmQ, &q_full[qb], qc, ui.q_row0, kEvictFirst);
-          tma_load_2d(dst + AT_QBOX, &tmQ, &q_full[qb], qc + 64, ui.q_row0, kEvictFirst);
+          for (int x = 0; x < NBX; ++x)
+            tma_load_2d(dst + x * AT_QBOX, &tmQ, &q_full[qb], qc + 64 * x, ui.q_row0, kEvictFirst);
         }
       }
       __syncwarp();
@@ -165,10 +179,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         uint8_t* dst = sKV + st * AT_KV_STAGE;
         if (elect_one()) {
           mbar_arrive_expect_tx(&kv_full[st], AT_KV_STAGE);
-          tma_load_2d(dst, &tmKV, &kv_full[st], kc, krow, kEvictLast);
-          tma_load_2d(dst + AT_KBOX, &tmKV, &kv_full[st], kc + 64, krow, kEvictLast);
-          tma_load_2d(dst + 2 * AT_KBOX, &tmKV, &kv_full[st], vc, krow, kEvictLast);
-          tma_load_2d(dst + 3 * AT_KBOX, &tmKV, &kv_full[st], vc + 64, krow, kEvictLast);
+          for (int x = 0; x < NBX; ++x) {
+            tma_load_2d(dst + x * AT_KBOX, &tmKV, &kv_full[st], kc + 64 * x, krow, kEvictLast);
+            tma_load_2d(dst + (NBX + x) * AT_KBOX, &tmKV, &kv_full[st], vc + 64 * x, krow, kEvictLast);
+          }
         }
         __syncwarp();
       }
@@ -179,14 +193,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     // Software-pipelined: once softmax_j has consumed S_j(b) (p_ready), S_j(b+1) is issued ahead
     // of PV_j(b), so the tensor core computes the next scores while softmax_j waits for nothing.
     constexpr uint32_t idesc_s = make_idesc_bf16(128, AT_KB, false, false);
-    constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);   // V is MN-major
+    constexpr uint32_t idesc_o = make_idesc_bf16(128, DH, false, true);    // V is MN-major
     uint32_t kv_it = 0, q_it = 0, blk0 = 0, blk1 = 0;
     const uint64_t q_desc = kmajor_desc(smem_u32(sQ));
     int k = 0;
     auto issue_s = [&](int j, uint32_t st) {
       const uint64_t k_desc = kmajor_desc(smem_u32(sKV + st * AT_KV_STAGE));
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {   // descriptor start field is in 16-byte units
+      for (int kk = 0; kk < DH / 16; ++kk) {   // descriptor start field is in 16-byte units
         const uint32_t qo = (j * AT_Q_HEAD + (kk >> 2) * AT_QBOX + (kk & 3) * 32) >> 4;
         const uint32_t ko = ((kk >> 2) * AT_KBOX + (kk & 3) * 32) >> 4;
         umma_bf16_ss(tmem_base + AT_TS + j * AT_KB, q_desc + qo, k_desc + ko, idesc_s, kk != 0);
@@ -215,7 +229,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           mbar_wait(&kv_full[st_n], ((kv_it + b + 1) / AT_STAGES) & 1);
           att_trace(EV_KVFULL, k, b + 1, 9);
         }
-        const uint32_t v_addr = smem_u32(sKV + st_b * AT_KV_STAGE) + 2 * AT_KBOX;
+        const uint32_t v_addr = smem_u32(sKV + st_b * AT_KV_STAGE) + NBX * AT_KBOX;
         for (int j = 0; j < ui.nh; ++j) {
           uint32_t& bi = j == 0 ? blk0 : blk1;
           const uint32_t pbuf = bi & 1;
@@ -230,7 +244,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             }
 #pragma unroll
             for (int kk = 0; kk < AT_KB / 16; ++kk) {
-              umma_bf16_ts(tmem_base + AT_TO + j * 128, tmem_base + AT_TP + j * 64 + pbuf * 32 + kk * 8,
+              umma_bf16_ts(tmem_base + AT_TO + j * DH, tmem_base + AT_TP + j * 64 + pbuf * 32 + kk * 8,
                            sw128_desc(v_addr + kk * 2048, AT_KBOX, 1024), idesc_o, (b | kk) != 0);
             }
             umma_commit(&pv_done[j]);
@@ -250,7 +264,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const uint32_t row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
     const uint32_t tS = tmem_base + lane_base + AT_TS + j * AT_KB;
-    const uint32_t tO = tmem_base + lane_base + AT_TO + j * 128;
+    const uint32_t tO = tmem_base + lane_base + AT_TO + j * DH;
     const uint32_t tP = tmem_base + lane_base + AT_TP + j * 64;
     const float sl2 = d.scale * 1.4426950408889634f;
     uint32_t blk_it = 0, u_it = 0;
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             const float alpha = exp2f(m_used - m_new);
             l_run *= alpha;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < DH / 32; ++c) {
               uint32_t o[32];
               tmem_ld_32x32b_x32(tO + c * 32, o);
               tmem_ld_wait();
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(d.out) +
                                             (size_t)(ui.q_row0 + row) * (d.H * d.dh) + (ui.h0 + j) * d.dh);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < DH / 32; ++c) {
         uint32_t o[32];
         tmem_ld_32x32b_x32(tO + c * 32, o);
         tmem_ld_wait();
@@ -372,8 +386,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         if (lane == 0) {
           const int r0 = ui.q_row0 + (warp & 3) * 32;
           const int c0 = (ui.h0 + j) * d.dh;
-          tma_store_2d(&tmO, ost, c0, r0);
-          tma_store_2d(&tmO, ost + 4096, c0 + 64, r0);
+          for (int x = 0; x < NBX; ++x) tma_store_2d(&tmO, ost + x * 4096, c0 + 64 * x, r0);
           tma_store_commit();
         }
       }
@@ -402,32 +415,38 @@ int debug_set_attention_trace(unsigned long long* buf, unsigned int cap) {
 
 static int g_att_sms = 0;
 
-int launch_attention(const AttnDesc& d, cudaStream_t stream) {
-  if (d.dh != 128) return fail(-2, "attention: d_head must be 128 (got %d)", d.dh);
-  if (d.H % d.Hkv != 0) return fail(-2, "attention: n_heads %% n_kv_heads != 0");
-  if (d.n_work == 0) return 0;
+template <int DH>
+static int launch_attention_t(const AttnDesc& d, cudaStream_t stream) {
   const int ldq = (d.H + 2 * d.Hkv) * d.dh;
-  CUtensorMap tq, tkv;
+  CUtensorMap tq, tkv, to;
   if (!make_tmap_2d(&tq, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, 128, 64, true)) return -3;
   if (!make_tmap_2d(&tkv, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, AT_KB, 64, true)) return -3;
-  CUtensorMap to;
   const int ldo = d.H * d.dh;
   if (!make_tmap_2d(&to, d.out, 2, (uint64_t)d.T, (uint64_t)ldo, (uint64_t)ldo, 32, 64, true)) return -3;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
+    cudaFuncSetAttribute(attn_prefix_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, AtCfg<DH>::SMEM);
+    attr_set = true;
+  }
+  if (g_att_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_att_sms, cudaDevAttrMultiProcessorCount, dev);
-    attr_set = true;
   }
   const int r = d.H / d.Hkv;
   const int n_units = d.n_work * d.Hkv * ((r + 1) / 2);
   const int grid = n_units < g_att_sms ? n_units : g_att_sms;
-  attn_prefix_kernel<<<grid, AT_THREADS, AT_SMEM, stream>>>(tq, tkv, to, d, n_units);
+  attn_prefix_kernel<DH><<<grid, AT_THREADS, AtCfg<DH>::SMEM, stream>>>(tq, tkv, to, d, n_units);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(-4, "attention launch: %s", cudaGetErrorString(e));
   return 0;
+}
+
+int launch_attention(const AttnDesc& d, cudaStream_t stream) {
+  if (d.dh != 128 && d.dh != 64) return fail(-2, "attention: d_head must be 64 or 128 (got %d)", d.dh);
+  if (d.H % d.Hkv != 0) return fail(-2, "attention: n_heads %% n_kv_heads != 0");
+  if (d.n_work == 0) return 0;
+  return d.dh == 128 ? launch_attention_t<128>(d, stream) : launch_attention_t<64>(d, stream);
 }
 
 }  // namespace pf

@@ -146,7 +146,8 @@ int pf_model_create(const pf_model_desc* desc, pf_model** out) {
       d.n_heads % d.n_kv_heads != 0)
     return fail(-2, "pf_model_create: invalid dims (L=%d d=%d H=%d Hkv=%d)", d.n_layers, d.d_model,
                 d.n_heads, d.n_kv_heads);
-  if (d.d_head != 128) return fail(-2, "pf_model_create: d_head must be 128 (got %d)", d.d_head);
+  if (d.d_head != 128 && d.d_head != 64)
+    return fail(-2, "pf_model_create: d_head must be 64 or 128 (got %d)", d.d_head);
   if (d.d_ff_pad % 128 != 0 || d.d_ff_pad < d.d_ff)
     return fail(-2, "pf_model_create: d_ff_pad=%d must be a multiple of 128 >= d_ff=%d", d.d_ff_pad, d.d_ff);
   pf_model* m = new (std::nothrow) pf_model();
@@ -211,7 +212,7 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     g.A = w.xb; g.lda = d.d_model; g.B = d.w_qkv[l]; g.ldb = d.d_model;
     g.C = w.qkv; g.ldc = m->qkv_n; g.M = T; g.N = m->qkv_n; g.K = d.d_model;
     g.epilogue = EPI_ROPE_BF16; g.pos = pos; g.rope_cos = d.rope_cos; g.rope_sin = d.rope_sin;
-    g.rope_heads = d.n_heads + d.n_kv_heads; g.max_seq = d.max_seq;
+    g.rope_heads = d.n_heads + d.n_kv_heads; g.rope_dh = d.d_head; g.max_seq = d.max_seq;
     g.row_ss = w.ss_attn; g.ss_zero = w.ss_mlp; g.inv_d = inv_d; g.eps = eps;
     if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
     AttnDesc a{};
@@ -336,6 +337,7 @@ int pf_gemm_bf16_ex(const pf_gemm_args* a, pf_stream_t stream) {
   g.A = a->A; g.lda = a->lda; g.B = a->B; g.ldb = a->ldb; g.C = a->C; g.ldc = a->ldc;
   g.M = a->M; g.N = a->N; g.K = a->K; g.epilogue = a->epilogue;
   g.pos = a->pos; g.rope_cos = a->rope_cos; g.rope_sin = a->rope_sin; g.rope_heads = a->rope_heads;
+  g.rope_dh = a->rope_dh;
   g.row_ss = a->row_ss; g.ss_zero = a->ss_zero; g.ss_out = a->ss_out; g.xb = a->xb; g.ldxb = a->ldxb;
   g.inv_d = a->inv_d; g.eps = a->eps;
   return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));

@@ -53,7 +53,8 @@ struct GemmArgs {
   const int32_t* pos;      // EPI_ROPE: position per row
   const float* rope_cos;   // [max_seq x 64]
   const float* rope_sin;
-  int rope_heads;          // heads (of 128 cols) that receive RoPE
+  int rope_heads;          // heads (of rope_dh cols) that receive RoPE
+  int rope_dh;             // head width: 64 or 128
   const float* row_ss;     // fused RMSNorm: per-row sum of squares of the residual (or null)
   float* ss_zero;          // rows to clear (n-tile 0) for the next accumulation (or null)
   float* ss_out;           // EPI_RESID_ADD_NORM: per-row sum of squares accumulator
@@ -379,24 +380,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           emit(w, n0 / 2 + c * 64, r0);
         }
       } else {  // EPI_ROPE_BF16
-        // Rotate-half RoPE: head column i pairs with i+64.  For each 32-column half c the thread
-        // loads x1 = cols [32c, 32c+32) and x2 = cols [64+32c, ...); rotated x1 lands in the
-        // "lo" 64-col box (16-byte chunks 4c..4c+3), rotated x2 in the "hi" box.
+        // Rotate-half RoPE on heads of width dh (64 or 128): head column e pairs with e + dh/2.
+        // For each 32-column block c of the first half the thread loads x1 = cols [32c, 32c+32)
+        // and x2 = cols [dh/2 + 32c, ...); outputs land in 64-column SW128 boxes (dh/64 per head).
+        const int dh = args.rope_dh;
+        const int half = dh / 2;
         const int p = rvalid ? __ldg(args.pos + grow) : 0;
-        const float4* cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * 64);
-        const float4* sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * 64);
-        const uint32_t stg_lo = smem_u32(my_stg);
-        const uint32_t stg_hi = smem_u32(my_stg + GEMM_STG_BYTES);
+        const float4* cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * half);
+        const float4* sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
+        const uint32_t stg0 = smem_u32(my_stg);
 #pragma unroll 1
-        for (int hd = 0; hd < GEMM_BN / 128; ++hd) {
-          const bool rot = ((n0 + hd * 128) / 128) < args.rope_heads;
+        for (int hd = 0; hd < GEMM_BN / dh; ++hd) {
+          const bool rot = ((n0 + hd * dh) / dh) < args.rope_heads;
           if (lane == 0) tma_store_wait_read<0>();
           __syncwarp();
 #pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < half / 32; ++c) {
             uint32_t x1[32], x2[32];
-            tmem_ld_32x32b_x32(t_row + hd * 128 + c * 32, x1);
-            tmem_ld_32x32b_x32(t_row + hd * 128 + 64 + c * 32, x2);
+            tmem_ld_32x32b_x32(t_row + hd * dh + c * 32, x1);
+            tmem_ld_32x32b_x32(t_row + hd * dh + half + c * 32, x2);
             tmem_ld_wait();
             uint32_t w1[16], w2[16];
 #pragma unroll
@@ -418,18 +420,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               w2[j4 * 2] = pack_bf16x2(o2[0], o2[1]);
               w2[j4 * 2 + 1] = pack_bf16x2(o2[2], o2[3]);
             }
+            const int e1 = c * 32, e2 = half + c * 32;   // head-local first column of each part
+            const uint32_t b1 = stg0 + (e1 / 64) * GEMM_STG_BYTES + lane * 128;
+            const uint32_t b2 = stg0 + (e2 / 64) * GEMM_STG_BYTES + lane * 128;
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
-              const uint32_t off = lane * 128 + (((c * 4 + q4) ^ (lane & 7)) << 4);
-              st_shared_v4(stg_lo + off, w1[4 * q4], w1[4 * q4 + 1], w1[4 * q4 + 2], w1[4 * q4 + 3]);
-              st_shared_v4(stg_hi + off, w2[4 * q4], w2[4 * q4 + 1], w2[4 * q4 + 2], w2[4 * q4 + 3]);
+              const uint32_t k1 = (e1 % 64) / 8 + q4, k2 = (e2 % 64) / 8 + q4;
+              st_shared_v4(b1 + ((k1 ^ (lane & 7)) << 4), w1[4 * q4], w1[4 * q4 + 1], w1[4 * q4 + 2], w1[4 * q4 + 3]);
+              st_shared_v4(b2 + ((k2 ^ (lane & 7)) << 4), w2[4 * q4], w2[4 * q4 + 1], w2[4 * q4 + 2], w2[4 * q4 + 3]);
             }
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, my_stg, n0 + hd * 128, r0);
-            tma_store_2d(&tmC, my_stg + GEMM_STG_BYTES, n0 + hd * 128 + 64, r0);
+            for (int x = 0; x < dh / 64; ++x)
+              tma_store_2d(&tmC, my_stg + x * GEMM_STG_BYTES, n0 + hd * dh + 64 * x, r0);
             tma_store_commit();
           }
         }
@@ -555,6 +560,7 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
   a.M = d.M; a.N = d.N; a.K = d.K;
   a.num_n_blk = (d.N + GEMM_BN - 1) / GEMM_BN;
   a.pos = d.pos; a.rope_cos = d.rope_cos; a.rope_sin = d.rope_sin; a.rope_heads = d.rope_heads;
+  a.rope_dh = d.rope_dh == 64 ? 64 : 128;
   a.row_ss = d.row_ss; a.ss_zero = d.ss_zero; a.ss_out = d.ss_out;
   a.resid = reinterpret_cast<const float*>(d.C); a.ldr = d.ldc;
   a.xb_out = d.xb; a.ldxb = d.ldxb;

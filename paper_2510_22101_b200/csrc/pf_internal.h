@@ -39,6 +39,7 @@ struct GemmDesc {
   const float* rope_cos;
   const float* rope_sin;
   int rope_heads;
+  int rope_dh;     // head width for the RoPE epilogue (64 or 128; 0 -> 128)
   int max_seq;
   // fused RMSNorm (see gemm.cu): A rows are bf16(residual); the epilogue multiplies row r by
   // rsqrt(row_ss[r]/d + eps).  ss_zero rows are cleared by the n-tile-0 CTAs (for the next

@@ -132,8 +132,8 @@ def attention_ref(qkv, packed, H, Hkv, dh=128):
     return out.view(T, H * dh)
 
 
-@pytest.mark.parametrize("H,Hkv", [(2, 1), (4, 2), (10, 5)])
-def test_prefix_attention(lib, H, Hkv):
+@pytest.mark.parametrize("H,Hkv,dh", [(2, 1, 128), (4, 2, 128), (10, 5, 128), (4, 2, 64), (2, 2, 64)])
+def test_prefix_attention(lib, H, Hkv, dh):
     rng = np.random.default_rng(0)
     reqs = [
         SharedBatch(list(rng.integers(16, 100, 64)), [list(rng.integers(16, 100, s)) for s in (100, 128, 200, 1, 300)]),
@@ -143,14 +143,14 @@ def test_prefix_attention(lib, H, Hkv):
     ]
     packed = pack_requests(reqs)
     T = packed.T
-    qkv = rand_bf16(T, (H + 2 * Hkv) * 128, seed=11)
-    out = torch.full((T, H * 128), float("nan"), device="cuda", dtype=torch.bfloat16)
+    qkv = rand_bf16(T, (H + 2 * Hkv) * dh, seed=11)
+    out = torch.full((T, H * dh), float("nan"), device="cuda", dtype=torch.bfloat16)
     segs = torch.from_numpy(packed.segs).cuda()
     work = torch.from_numpy(packed.work).cuda()
-    rc = lib.pf_prefix_attention(P(qkv), P(out), T, H, Hkv, 128, P(segs), P(work), len(packed.work), stream())
+    rc = lib.pf_prefix_attention(P(qkv), P(out), T, H, Hkv, dh, P(segs), P(work), len(packed.work), stream())
     _lib.check(rc)
     torch.cuda.synchronize()
-    ref = attention_ref(qkv, packed, H, Hkv)
+    ref = attention_ref(qkv, packed, H, Hkv, dh)
     torch.testing.assert_close(out.float(), ref, rtol=2e-2, atol=2e-2)
 
 
@@ -247,3 +247,19 @@ def test_gemm_row_scaled_swiglu_and_rope(lib):
             pos=pos, rope_cos=cos, rope_sin=sin, rope_heads=3, row_ss=ss_in, inv_d=1.0 / K, eps=1e-6)
     refq = rope_ref(xn @ Bq.float().t(), pos, cos, sin, 3)
     torch.testing.assert_close(Cq.float(), refq, rtol=1.6e-2, atol=2e-2)
+
+
+def test_gemm_rope_dh64(lib):
+    """RoPE epilogue on 64-wide heads (config C1: d_head = d_model / n_heads = 64)."""
+    M, K, H, Hkv = 700, 256, 4, 2
+    cfg = ModelConfig(n_layers=1, d_model=K, n_heads=H, n_kv_heads=Hkv, d_ff=128, d_head=64)
+    cos, sin = (torch.from_numpy(t).cuda() for t in rope_tables(cfg))
+    N = (H + 2 * Hkv) * 64
+    A = rand_bf16(M, K, seed=40)
+    B = rand_bf16(N, K, scale=K ** -0.5, seed=41)
+    pos = torch.randint(0, cfg.max_seq, (M,), device="cuda", dtype=torch.int32)
+    C = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    gemm_ex(lib, A=A, lda=K, B=B, ldb=K, C=C, ldc=N, M=M, N=N, K=K, epilogue=_lib.EPI_ROPE_BF16,
+            pos=pos, rope_cos=cos, rope_sin=sin, rope_heads=H + Hkv, rope_dh=64)
+    ref = rope_ref(A.float() @ B.float().t(), pos, cos, sin, H + Hkv, dh=64)
+    torch.testing.assert_close(C.float(), ref, rtol=1.6e-2, atol=2e-2)

@@ -56,7 +56,7 @@ def get_models(name, seed=0):
     return _models[name]
 
 
-@pytest.mark.parametrize("name", ["TINY", "TINY_GQA"])
+@pytest.mark.parametrize("name", ["TINY", "TINY_GQA", "C1"])
 @pytest.mark.parametrize("family", ["template", "spread"])
 def test_model_parity_small(name, family):
     cfg, scorer, ow = get_models(name)
@@ -80,6 +80,21 @@ def test_model_parity_small(name, family):
         ties += check_request_topk(p_ref[off:off + n], res.p_yes[off:off + n], family, max_dp)
         off += n
     print(f"near-ties declared: {ties}")
+
+
+def test_c1_exact_request():
+    """BASELINE config 1 (C1): 2 layers, d=256, 4 heads (d_head 64): 1 query x 32 items x
+    128-token suffix, prefix 64, scored on the GPU against the CPU oracle."""
+    cfg, scorer, ow = get_models("C1")
+    for family in ("template", "spread"):
+        rng = np.random.default_rng(100)
+        batches = [make_shared(rng, 64, [128] * 32, family)]
+        res = score_shared_batch(scorer, batches)
+        p_ref = oracle_scores(ow, batches)
+        max_dp = float(np.max(np.abs(res.p_yes - p_ref)))
+        print(f"C1/{family}: max|dp|={max_dp:.2e}")
+        assert max_dp <= TOL_P
+        check_request_topk(p_ref, res.p_yes, family, max_dp)
 
 
 def test_single_item_and_no_prefix():
