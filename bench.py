@@ -337,13 +337,120 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- C5 mixed load
+def c5_request(rng, cfg, prefix_len=64):
+    """items ~U{10..500}, item tokens ~U{64..1024}, 64-token query prefix."""
+    from paper_2510_22101_b200 import SharedBatch
+
+    n = int(rng.integers(10, 501))
+    prefix = [3] + [int(x) for x in rng.integers(16, cfg.vocab_size, prefix_len - 1)]
+    sufs = []
+    for s_len in rng.integers(64, 1025, n):
+        suf = rng.integers(16, cfg.vocab_size, int(s_len)).astype(np.int64)
+        suf[-1] = 11
+        sufs.append(suf.tolist())
+    return SharedBatch(prefix, sufs)
+
+
+def nearest_rank(sorted_vals, q):
+    """Nearest-rank percentile."""
+    if not sorted_vals:
+        return None
+    k = max(1, int(np.ceil(q / 100.0 * len(sorted_vals))))
+    return sorted_vals[k - 1]
+
+
+def run_load(args):
+    """Open-loop Poisson load on one GPU: requests arrive at seeded exponential
+    gaps; a serving loop packs every request that has arrived (up to a token budget) into one
+    pf_score call; latency = completion - arrival (wall clock, includes packing, H2D, D2H)."""
+    import torch
+
+    from paper_2510_22101_b200 import CONFIGS, init_device_weights, pack_requests
+    from paper_2510_22101_b200.engine import PrefillScorer
+
+    cfg = CONFIGS["C4"]
+    torch.cuda.set_device(0)
+    scorer = PrefillScorer(init_device_weights(cfg, 0, "cuda"), device="cuda")
+    rng = np.random.default_rng(args.seed)
+    pool = [c5_request(rng, cfg) for _ in range(args.load_pool)]
+    items_per_req = float(np.mean([r.n_items for r in pool]))
+    tok_per_req = float(np.mean([len(r.prefix_tokens) + sum(len(s) for s in r.suffixes) for r in pool]))
+    budget = args.load_token_budget
+
+    def serve(batch):
+        return scorer.score_packed(pack_requests(batch, cfg.max_seq))
+
+    for r in pool[:3]:      # warm-up (kernel attributes, workspace growth)
+        serve([r])
+    # capacity: the whole pool back to back, packed up to the token budget
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    i = 0
+    while i < len(pool):
+        batch, toks = [], 0
+        while i < len(pool) and (not batch or toks + tok_per_req <= budget):
+            batch.append(pool[i]); toks += tok_per_req; i += 1
+        serve(batch)
+    cap_s = time.perf_counter() - t0
+    capacity = sum(r.n_items for r in pool) / cap_s
+
+    runs = []
+    for frac in args.load_fracs:
+        rate = frac * capacity / items_per_req             # requests/s
+        arng = np.random.default_rng(args.seed + int(frac * 1000))
+        n_req = max(8, int(rate * args.load_seconds))
+        arrivals = np.cumsum(arng.exponential(1.0 / rate, n_req))
+        reqs = [pool[k % len(pool)] for k in range(n_req)]
+        done = np.zeros(n_req)
+        start = time.perf_counter()
+        nxt = 0
+        queue = []
+        while nxt < n_req or queue:
+            now = time.perf_counter() - start
+            while nxt < n_req and arrivals[nxt] <= now:
+                queue.append(nxt); nxt += 1
+            if not queue:
+                time.sleep(max(0.0, min(arrivals[nxt] - now, 0.01)))
+                continue
+            batch, toks = [], 0
+            while queue and (not batch or toks + tok_per_req <= budget):
+                batch.append(queue.pop(0)); toks += tok_per_req
+            serve([reqs[k] for k in batch])
+            t_done = time.perf_counter() - start
+            for k in batch:
+                done[k] = t_done
+        lat = sorted(((done - arrivals) * 1e3).tolist())
+        wall = done.max() - arrivals[0]
+        runs.append({"offered_frac": frac, "offered_items_per_s": frac * capacity,
+                     "achieved_items_per_s": sum(r.n_items for r in reqs) / wall,
+                     "requests": n_req, "p50_ms": nearest_rank(lat, 50), "p90_ms": nearest_rank(lat, 90),
+                     "p95_ms": nearest_rank(lat, 95), "p99_ms": nearest_rank(lat, 99)})
+    line = {
+        "metric": METRIC, "value": runs[-1]["achieved_items_per_s"], "unit": "items/s", "n_gpus": 1,
+        "steps": sum(r["requests"] for r in runs), "warmup": 3, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic C5 mix (seeded): items ~U{10..500}, item tokens ~U{64..1024}, prefix 64; Poisson arrivals",
+        "config": {"workload": "C5 mixed load on the C4 model (1.7B-shaped, pruned 40%)",
+                   "mean_items_per_request": items_per_req, "mean_tokens_per_request": tok_per_req,
+                   "token_budget_per_launch": budget, "latency": "wall clock, arrival -> scores on host"},
+        "capacity_items_per_s": capacity, "load_runs": runs,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4"])
+    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--seed", type=int, default=5)
+    ap.add_argument("--load-pool", type=int, default=24)
+    ap.add_argument("--load-seconds", type=float, default=20.0)
+    ap.add_argument("--load-fracs", type=float, nargs="+", default=[0.5, 0.8])
+    ap.add_argument("--load-token-budget", type=int, default=262144)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-items", type=int, default=2)
@@ -351,6 +458,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "C5":
+        run_load(args)
     else:
         run_ours(args)
 
