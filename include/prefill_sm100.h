@@ -125,6 +125,28 @@ PF_API int pf_head_last_token(const float* resid, const int32_t* last_idx, int n
                        float eps, float* logits2, float* p_yes, int* bad_flag,
                        pf_stream_t stream);
 
+/* ---- Host ingest (C++, no GPU needed) ------------------------------
+ * FNV-1a-64 word-hash tokenizer, bit-identical to prefrank tokenizer.encode
+ * (/root/reference/pkg/src/prefrank/tokenizer.py:119-134).  UTF-8 input; ids written to out_ids
+ * (at most cap; *n_out = total count, -5 if it exceeded cap).  vocab_size/reserved as Vocab. */
+PF_API int pf_tokenize(const char* text, size_t len, int vocab_size, int reserved, int32_t* out_ids,
+                       int64_t cap, int64_t* n_out);
+/* Batched (tokenizer.py:137-161 encode_batch): texts are data[text_offsets[i]..text_offsets[i+1]);
+ * cap must be >= total input bytes; out_offsets[n_texts+1] delimits each text's ids.
+ * n_threads <= 0 uses all hardware threads. */
+PF_API int pf_tokenize_batch(const char* data, const int64_t* text_offsets, int n_texts, int vocab_size,
+                             int reserved, int32_t* out_ids, int64_t cap, int64_t* out_offsets,
+                             int n_threads);
+/* split_shared_prefix + flat packing, bit-identical to prefixcache.pack_requests.
+ * Request r owns token lists [list_begin[r], list_begin[r+1]) of the flat list set
+ * ids[list_offsets[k]..list_offsets[k+1]).  pf_pack_sizes gives buffer upper bounds. */
+PF_API int pf_pack_sizes(const int64_t* list_offsets, const int32_t* list_begin, int n_requests,
+                         int64_t* T, int64_t* n_seg, int64_t* n_items);
+PF_API int pf_pack_requests(const int32_t* ids, const int64_t* list_offsets, const int32_t* list_begin,
+                            int n_requests, int max_seq, int32_t* out_ids, int32_t* out_pos,
+                            int32_t* out_segs, int32_t* out_last, int32_t* out_prefix_lens,
+                            int64_t* out_T, int64_t* out_n_seg);
+
 /* Debug hook: CTA 0 of the attention kernel appends {event, role, unit, block, globaltimer}
  * records (uint64) to device_buf (NULL disables).  Used by tools/attn_trace.py. */
 PF_API int pf_debug_set_trace(void* device_buf, unsigned int capacity);

@@ -21,6 +21,8 @@ REF = "/root/reference/pkg/src"
 if REF not in sys.path:
     sys.path.insert(0, REF)
 
+import random  # noqa: E402
+
 from prefrank import corpus, tokenizer  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "prompts.json")
@@ -51,7 +53,21 @@ def main():
         budget_err = None
     except corpus.PromptBudgetError as e:
         budget_err = str(e)
+    # tokenizer known answers on adversarial texts: case, punctuation, tag spellings, Unicode whose
+    # lowercase is ASCII (U+0130, U+212A), other scripts, combining marks, emoji
+    frng = random.Random(2510)
+    alphabet = (list("abcxyzABCXYZ0189 _-.,;:!?|<>/\\'\"()[]{}\t\n") + ["<|sys|>", "<|/SYS|>", "<|Q|>", "<|/q|>",
+                "<|meta|>", "<|/meta|>", "<|desc|>", "<|/desc|>", "<|ANS|>", "<|ans", "|>", "<|",
+                "\u0130", "\u212a", "\u00df", "\u00c9", "\u0131", "\u03a3", "\u4e2d\u6587", "\u0307",
+                "\U0001F600", "yes", "no", "Yes", "NO", "rust", "Engineer"])
+    fuzz = ["".join(frng.choice(alphabet) for _ in range(frng.randint(0, 60))) for _ in range(400)]
+    fuzz += ["", "   ", "\u0130stanbul KELVIN \u212a", "<|ans|><|ans|>", "a<|q|>b", "x" * 300]
+    prompt_texts = []
+    for qi, q in enumerate(queries[:2]):
+        for it in items[qi * 8: qi * 8 + 3]:
+            prompt_texts.append(corpus.truncate_description(corpus.assemble_prompt(q, it), 2048, vocab).full_prompt())
     golden = {
+        "texts": [[t, enc(t)] for t in fuzz + prompt_texts],
         "generator": "tests/golden/make_golden.py (reference prefrank tokenizer.py + corpus.py)",
         "fnv": {"offset": tokenizer.FNV_OFFSET, "prime": tokenizer.FNV_PRIME,
                 "fnv1a_64": {w: tokenizer.fnv1a_64(w.encode()) for w in ["rust", "engineer", "a", ""]}},

@@ -190,6 +190,20 @@ def test_trained_norm_gains_parity():
     assert np.max(np.abs(res.p_yes - p_ref)) <= TOL_P
 
 
+def test_checkpoint_to_device_matches(tmp_path):
+    """PRLK checkpoint streamed to the device scores bit-identically to the in-memory weights."""
+    from paper_2510_22101_b200.checkpoint import load_checkpoint_to_device, save_checkpoint
+
+    cfg = CONFIGS["TINY_GQA"]
+    w = init_weights(cfg, 4)
+    save_checkpoint(w, str(tmp_path / "m.prlk"))
+    rng = np.random.default_rng(2)
+    packed = pack_requests([make_shared(rng, 30, list(rng.integers(1, 150, 12)), "spread")])
+    a = PrefillScorer(w).score_packed(packed)
+    b = PrefillScorer(load_checkpoint_to_device(str(tmp_path / "m.prlk"))).score_packed(packed)
+    np.testing.assert_array_equal(a.p_yes, b.p_yes)
+
+
 def test_graph_replay_matches_direct():
     from paper_2510_22101_b200.engine import DevicePacked
 
