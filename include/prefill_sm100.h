@@ -131,6 +131,10 @@ PF_API int pf_head_last_token(const float* resid, const int32_t* last_idx, int n
  * (at most cap; *n_out = total count, -5 if it exceeded cap).  vocab_size/reserved as Vocab. */
 PF_API int pf_tokenize(const char* text, size_t len, int vocab_size, int reserved, int32_t* out_ids,
                        int64_t cap, int64_t* n_out);
+/* Same, plus the end of each token's span in the lowercased text, in Python str units (the span
+ * end tokenizer.encode_with_spans reports, tokenizer.py:104-116; used by truncate_description). */
+PF_API int pf_tokenize_spans(const char* text, size_t len, int vocab_size, int reserved, int32_t* out_ids,
+                             int64_t* out_ends, int64_t cap, int64_t* n_out);
 /* Batched (tokenizer.py:137-161 encode_batch): texts are data[text_offsets[i]..text_offsets[i+1]);
  * cap must be >= total input bytes; out_offsets[n_texts+1] delimits each text's ids.
  * n_threads <= 0 uses all hardware threads. */

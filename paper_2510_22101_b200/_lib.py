@@ -23,7 +23,7 @@ EXPORTED_SYMBOLS = (
     "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host",
     "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
     "pf_last_error", "pf_version", "pf_debug_set_trace",
-    "pf_tokenize", "pf_tokenize_batch", "pf_pack_sizes", "pf_pack_requests",
+    "pf_tokenize", "pf_tokenize_spans", "pf_tokenize_batch", "pf_pack_sizes", "pf_pack_requests",
 )
 
 
@@ -89,6 +89,7 @@ _SIGS = {
     "pf_head_last_token": (_I, [_P, _P, _I, _I, _P, _P, _P, _F, _P, _P, _P, _P]),
     "pf_debug_set_trace": (_I, [_P, ctypes.c_uint]),
     "pf_tokenize": (_I, [ctypes.c_char_p, ctypes.c_size_t, _I, _I, _P, ctypes.c_int64, _P]),
+    "pf_tokenize_spans": (_I, [ctypes.c_char_p, ctypes.c_size_t, _I, _I, _P, _P, ctypes.c_int64, _P]),
     "pf_tokenize_batch": (_I, [_P, _P, _I, _I, _I, _P, ctypes.c_int64, _P, _I]),
     "pf_pack_sizes": (_I, [_P, _P, _I, _P, _P, _P]),
     "pf_pack_requests": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P]),

@@ -66,8 +66,10 @@ void lower_stream(const char* s, size_t n, std::string& out) {
 
 inline bool is_word(char c) { return (c >= 'a' && c <= 'z') || (c >= '0' && c <= '9'); }
 
+// ends (optional): end index of each token in the lowercased string, counted in Python str
+// units (code points; U+0130 counts 2), i.e. the span end tokenizer.encode_with_spans reports.
 int64_t tokenize_one(const char* text, size_t n, int32_t* out, int64_t cap, int size, int reserved,
-                     std::string& buf) {
+                     std::string& buf, int64_t* ends = nullptr) {
   lower_stream(text, n, buf);
   const char* s = buf.data();
   const size_t m = buf.size();
@@ -80,7 +82,10 @@ int64_t tokenize_one(const char* text, size_t n, int32_t* out, int64_t cap, int 
       bool hit = false;
       for (const TagSpec& t : kTags) {
         if (i + t.len <= m && std::memcmp(s + i, t.text, t.len) == 0) {
-          if (k < cap) out[k] = t.id;
+          if (k < cap) {
+            out[k] = t.id;
+            if (ends) ends[k] = static_cast<int64_t>(i + t.len);
+          }
           ++k;
           i += t.len;
           hit = true;
@@ -106,7 +111,10 @@ int64_t tokenize_one(const char* text, size_t n, int32_t* out, int64_t cap, int 
     if (len == 3 && s[i] == 'y' && s[i + 1] == 'e' && s[i + 2] == 's') id = 1;
     else if (len == 2 && s[i] == 'n' && s[i + 1] == 'o') id = 2;
     else id = static_cast<int32_t>(reserved + h % modulus);
-    if (k < cap) out[k] = id;
+    if (k < cap) {
+      out[k] = id;
+      if (ends) ends[k] = static_cast<int64_t>(j);
+    }
     ++k;
     i = j;
   }
@@ -123,6 +131,16 @@ int pf_tokenize(const char* text, size_t len, int vocab_size, int reserved, int3
   if (vocab_size <= reserved || reserved < 12) return -1;
   std::string buf;
   const int64_t k = tokenize_one(text, len, out_ids, cap, vocab_size, reserved, buf);
+  if (n_out) *n_out = k;
+  return k > cap ? -5 : 0;
+}
+
+int pf_tokenize_spans(const char* text, size_t len, int vocab_size, int reserved, int32_t* out_ids,
+                      int64_t* out_ends, int64_t cap, int64_t* n_out) {
+  if (!text && len) return -1;
+  if (vocab_size <= reserved || reserved < 12) return -1;
+  std::string buf;
+  const int64_t k = tokenize_one(text, len, out_ids, cap, vocab_size, reserved, buf, out_ends);
   if (n_out) *n_out = k;
   return k > cap ? -5 : 0;
 }

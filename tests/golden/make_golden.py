@@ -66,7 +66,24 @@ def main():
     for qi, q in enumerate(queries[:2]):
         for it in items[qi * 8: qi * 8 + 3]:
             prompt_texts.append(corpus.truncate_description(corpus.assemble_prompt(q, it), 2048, vocab).full_prompt())
+    from dataclasses import asdict
+    assembly = []
+    for qi, q in enumerate(queries[:2]):
+        for it in items[qi * 8: qi * 8 + 4]:
+            seg = corpus.assemble_prompt(q, it)
+            base = sum(len(enc(x)) for x in (seg.system_prefix, seg.query_text, seg.metadata_text, seg.suffix))
+            trunc = {}
+            for b in (base - 1, base, base + 1, base + 2, base + 3, base + 30, 300, 2048):
+                try:
+                    trunc[str(b)] = corpus.truncate_description(seg, b, vocab).full_prompt()
+                except corpus.PromptBudgetError as e:
+                    trunc[str(b)] = {"error": str(e)}
+            assembly.append({"query": asdict(q), "item": asdict(it), "segments": asdict(seg),
+                             "truncated": trunc})
+    spans = [[t, [list(x) for x in tokenizer.encode_with_spans(t, vocab)]] for t in fuzz[:100] + prompt_texts[:2]]
     golden = {
+        "assembly": assembly,
+        "spans": spans,
         "texts": [[t, enc(t)] for t in fuzz + prompt_texts],
         "generator": "tests/golden/make_golden.py (reference prefrank tokenizer.py + corpus.py)",
         "fnv": {"offset": tokenizer.FNV_OFFSET, "prime": tokenizer.FNV_PRIME,

