@@ -300,27 +300,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const float mx = sl2 * fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
                                      fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
         const bool need = mx > m_used + AT_RESCALE_THRESH;
-        if (__any_sync(0xffffffffu, need)) {
-          const float m_new = fmaxf(m_used, mx);
-          if (b > 0) {
-            // PV of the previous block may still be accumulating into O: wait for it.  (The
-            // parity is unambiguous: PV(blk_it-2) completed before S(blk_it) was issued.)
-            mbar_wait(&pv_done[j], (blk_it - 1) & 1);
-            tc_fence_after();
-            const float alpha = exp2f(m_used - m_new);
-            l_run *= alpha;
-#pragma unroll 1
-            for (int c = 0; c < DH / 32; ++c) {
-              uint32_t o[32];
-              tmem_ld_32x32b_x32(tO + c * 32, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st_32x32b_x32(tO + c * 32, o);
-            }
-          }
-          m_used = m_new;
-        }
+        const bool rescale = __any_sync(0xffffffffu, need);
+        const float m_old = m_used;
+        if (rescale) m_used = fmaxf(m_used, mx);
+        // P = exp2(s*scale - m_used) -> bf16 pairs -> TMEM (double-buffered; PV(n-1) read the other buffer)
         float sumv[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t w[32];
         const float neg_m = -m_used;
@@ -334,6 +317,24 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             w[c * 16 + i] = pack_bf16x2(p0, p1);   // TMEM A operand: 2 keys per 32-bit column
           }
         tmem_st_32x32b_x32(tP + (blk_it & 1) * 32, w);
+        // Every PV phase is consumed in order: PV of this head's previous block (issued right
+        // after this block's S) has finished by now, so this wait is ~free; it also guards O.
+        // (A unit's last PV phase is consumed in its epilogue.)
+        if (b > 0) mbar_wait(&pv_done[j], (blk_it - 1) & 1);
+        if (rescale && b > 0) {
+          tc_fence_after();
+          const float alpha = exp2f(m_old - m_used);
+          l_run *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_32x32b_x32(tO + c * 32, o);
+          }
+        }
         l_run += (sumv[0] + sumv[1]) + (sumv[2] + sumv[3]);
         tmem_st_wait();
         tc_fence_before();
@@ -343,6 +344,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       // ---- unit epilogue: O / l -> bf16 -> global
       mbar_wait(&o_done[j], u_it & 1);
+      mbar_wait(&pv_done[j], (blk_it - 1) & 1);
       if (lane == 0 && (warp & 3) == 0) att_trace(EV_ODONE, k, 0, j);
       ++u_it;
       tc_fence_after();
