@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();   // q/k/v come from the QKV GEMM
   auto unit = [&](int u, int k) { return k < AT_TAB ? tab[k] : decode_unit(d, u, r, n_pairs); };
 
   if (warp == 8) {
@@ -438,8 +440,19 @@ static int launch_attention_t(const AttnDesc& d, cudaStream_t stream) {
   const int r = d.H / d.Hkv;
   const int n_units = d.n_work * d.Hkv * ((r + 1) / 2);
   const int grid = n_units < g_att_sms ? n_units : g_att_sms;
-  attn_prefix_kernel<DH><<<grid, AT_THREADS, AtCfg<DH>::SMEM, stream>>>(tq, tkv, to, d, n_units);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(AT_THREADS);
+  cfg.dynamicSmemBytes = AtCfg<DH>::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_prefix_kernel<DH>, tq, tkv, to, d, n_units);
+  if (e != cudaSuccess) return fail(-4, "attention launch: %s", cudaGetErrorString(e));
+  e = cudaGetLastError();
   if (e != cudaSuccess) return fail(-4, "attention launch: %s", cudaGetErrorString(e));
   return 0;
 }

@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ 
                                                     const __nv_bfloat16* __restrict__ emb,
                                                     float* __restrict__ resid, uint4* __restrict__ xb,
                                                     float* __restrict__ ss, int T, int d) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -55,6 +57,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
                                                       __nv_bfloat16* __restrict__ y, int T,
                                                       float eps) {
   constexpr int d = NV * 128;
+  pdl_launch_dependents();
+  pdl_wait();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -90,6 +94,8 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ res
                                                    const float* __restrict__ w_no, float eps,
                                                    float* __restrict__ logits2,
                                                    float* __restrict__ p_yes, int* bad) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n_items) return;
@@ -121,6 +127,8 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restr
                                                           const uint4* __restrict__ attn, int attn_v4,
                                                           const float4* __restrict__ resid, int resid_v4,
                                                           uint4* __restrict__ attn_c, float4* __restrict__ resid_c) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n) return;

@@ -15,6 +15,9 @@ enum Epilogue : int {
   EPI_RESID_ADD_NORM = 4,   // resid += acc (fp32), xb = bf16(resid), ss_out[row] += sum(resid^2)
 };
 
+// ---- programmatic dependent launch switch (PF_NO_PDL=1 disables)
+bool pdl_enabled();
+
 // ---- error state (thread-local message, negative return codes; see include/prefill_sm100.h)
 void set_error(const char* fmt, ...);
 int fail(int code, const char* fmt, ...);

@@ -69,6 +69,14 @@ PF_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel is launched with programmaticStreamSerialization: it lets the next kernel in the
+// stream start (launch_dependents) once all its CTAs are resident, and waits (griddepcontrol.wait)
+// for the previous kernel's results only after its own prologue (TMEM alloc, barrier init,
+// descriptor prefetch).  Both are no-ops for a normal launch.
+PF_DEVICE void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+PF_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- fences
 PF_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
