@@ -89,7 +89,9 @@ PF_API int pf_score(pf_model* model, const int32_t* ids, const int32_t* pos, con
              int* bad_flag, pf_stream_t stream);
 
 /* Same, with HOST input/output buffers: H2D copies of the packed batch and D2H copy of the
- * scores are inside the call, which returns after the stream synchronises (-6 on non-finite). */
+ * scores are inside the call, which returns after the stream synchronises (-6 on non-finite).
+ * The host batch is validated first (ids < vocab, positions < max_seq, segments, work tiles and
+ * last_idx inside [0, T)); violations return -1 before any device work. */
 PF_API int pf_score_host(pf_model* model, const int32_t* ids, const int32_t* pos, const int32_t* segs,
                   int n_seg, const int32_t* work, int n_work, const int32_t* last_idx,
                   int n_items, int T, void* workspace, size_t ws_bytes, float* logits2_host,

@@ -297,6 +297,31 @@ int pf_score(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t*
                      p_yes, bad_flag, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// Host-side validation of a packed batch (pf_score_host only: the inputs are host memory).
+static int validate_packed(const pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+                           int n_seg, const int32_t* work, int n_work, const int32_t* last_idx, int n_items,
+                           int T) {
+  const pf_model_desc& d = m->d;
+  for (int t = 0; t < T; ++t) {
+    if (ids[t] < 0 || ids[t] >= d.vocab_size) return fail(-1, "token id %d at row %d outside vocab", ids[t], t);
+    if (pos[t] < 0 || pos[t] >= d.max_seq) return fail(-1, "position %d at row %d outside max_seq", pos[t], t);
+  }
+  for (int s = 0; s < n_seg; ++s) {
+    const int32_t* g = segs + 4 * s;
+    const int64_t kv_end = (int64_t)g[0] + g[1], q_end = (int64_t)g[2] + g[3];
+    if (g[0] < 0 || g[1] < 0 || g[2] < 0 || g[3] < 1 || kv_end > T || q_end > T)
+      return fail(-1, "segment %d {%d,%d,%d,%d} outside [0,%d)", s, g[0], g[1], g[2], g[3], T);
+  }
+  for (int w = 0; w < n_work; ++w) {
+    const int32_t* k = work + 4 * w;
+    if (k[0] < 0 || k[0] >= n_seg || k[1] < 0 || (int64_t)k[1] * 128 >= segs[4 * k[0] + 3])
+      return fail(-1, "work tile %d {%d,%d} invalid", w, k[0], k[1]);
+  }
+  for (int i = 0; i < n_items; ++i)
+    if (last_idx[i] < 0 || last_idx[i] >= T) return fail(-1, "last_idx[%d]=%d outside [0,%d)", i, last_idx[i], T);
+  return 0;
+}
+
 int pf_score_host(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
                   int n_seg, const int32_t* work, int n_work, const int32_t* last_idx, int n_items,
                   int T, void* workspace, size_t ws_bytes, float* logits2_host, float* p_yes_host,
@@ -304,6 +329,9 @@ int pf_score_host(pf_model* m, const int32_t* ids, const int32_t* pos, const int
   size_t need = 0;
   int rc = check_args(m, T, n_items, n_seg, n_work, workspace, ws_bytes, &need);
   if (rc) return rc;
+  if (!ids || !pos || !segs || !work || !last_idx || !logits2_host || !p_yes_host)
+    return fail(-1, "pf_score_host: null buffer");
+  if ((rc = validate_packed(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T))) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace w = layout(m, T, n_items, T, T, static_cast<uint8_t*>(workspace));
   cudaMemcpyAsync(w.ids, ids, (size_t)T * 4, cudaMemcpyHostToDevice, st);

@@ -204,6 +204,25 @@ def test_checkpoint_to_device_matches(tmp_path):
     np.testing.assert_array_equal(a.p_yes, b.p_yes)
 
 
+def test_host_path_rejects_malformed_batches():
+    from paper_2510_22101_b200 import _lib
+    from paper_2510_22101_b200.engine import PinnedPacked
+
+    cfg, scorer, _ = get_models("TINY")
+    rng = np.random.default_rng(6)
+    good = pack_requests([make_shared(rng, 8, [5, 9], "spread")])
+    for field, bad in (("ids", 99999), ("pos", 4096), ("last_idx", 10_000)):
+        pk = pack_requests([make_shared(rng, 8, [5, 9], "spread")])
+        getattr(pk, field)[0] = bad
+        with pytest.raises(_lib.PfError):
+            scorer.score_host(PinnedPacked(pk))
+    pk = pack_requests([make_shared(rng, 8, [5, 9], "spread")])
+    pk.segs[1, 3] = 10_000
+    with pytest.raises(_lib.PfError):
+        scorer.score_host(PinnedPacked(pk))
+    scorer.score_host(PinnedPacked(good))   # still healthy afterwards
+
+
 def test_graph_replay_matches_direct():
     from paper_2510_22101_b200.engine import DevicePacked
 
