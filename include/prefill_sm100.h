@@ -100,7 +100,8 @@ PF_API int pf_score_host(pf_model* model, const int32_t* ids, const int32_t* pos
 /* Per-op entry points (unit parity tests). */
 /* C = A[MxK] . B[NxK]^T (RoPE heads 128 wide here; pf_gemm_bf16_ex takes rope_dh 64/128)
  * with epilogue 0 bf16, 1 bf16+RoPE, 2 SwiGLU(bf16, N/2 cols),
- * 3 fp32 C += (residual add), 4 fp32 C += acc with xb = bf16(C) and ss_out[row] += sum(C^2). */
+ * 3 fp32 C += (residual add), 4 residual pair: x = xb + C held as bf16 (hi = xb, lo = C),
+ * updated in place to x + acc, and ss_out[row] += sum((x + acc)^2). */
 PF_API int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
                  int K, int epilogue, const int32_t* pos, const float* rope_cos,
                  const float* rope_sin, int rope_heads, pf_stream_t stream);
@@ -113,9 +114,10 @@ typedef struct pf_gemm_args {
   const float* row_ss; float* ss_zero; float* ss_out; void* xb; int ldxb; float inv_d, eps;
 } pf_gemm_args;
 PF_API int pf_gemm_bf16_ex(const pf_gemm_args* args, pf_stream_t stream);
-/* resid = float(E[ids]); optional xb = E[ids] (bf16) and ss = per-row sum of squares. */
-PF_API int pf_embed(const int32_t* ids, const void* emb, float* resid, void* xb, float* ss, int T, int d,
-             pf_stream_t stream);
+/* Embedding gather; every output is optional (NULL skips it): resid = float(E[ids]) (fp32),
+ * hi = E[ids] and lo = 0 (the bf16 residual pair the forward keeps), ss = per-row sum of squares. */
+PF_API int pf_embed(const int32_t* ids, const void* emb, float* resid, void* hi, void* lo, float* ss, int T,
+             int d, pf_stream_t stream);
 /* y = bf16(x * rsqrt(mean(x^2) + eps) * gamma); gamma may be NULL (all ones). */
 PF_API int pf_rmsnorm(const float* x, const float* gamma, void* y_bf16, int T, int d, float eps,
                pf_stream_t stream);

@@ -11,7 +11,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libprefill_sm100.so")
+LIB_PATH = os.environ.get("PF_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                          "libprefill_sm100.so")   # override: A/B builds only
 
 # Error codes (include/prefill_sm100.h)
 PF_EARG, PF_ESHAPE, PF_ETMAP, PF_ECUDA, PF_EWORKSPACE, PF_ENONFINITE = -1, -2, -3, -4, -5, -6
@@ -83,7 +84,7 @@ _SIGS = {
     "pf_score_host": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P]),
     "pf_gemm_bf16": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),
     "pf_gemm_bf16_ex": (_I, [ctypes.POINTER(PfGemmArgs), _P]),
-    "pf_embed": (_I, [_P, _P, _P, _P, _P, _I, _I, _P]),
+    "pf_embed": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "pf_rmsnorm": (_I, [_P, _P, _P, _I, _I, _F, _P]),
     "pf_prefix_attention": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _I, _P]),
     "pf_head_last_token": (_I, [_P, _P, _I, _I, _P, _P, _P, _F, _P, _P, _P, _P]),

@@ -95,15 +95,18 @@ constexpr size_t kAlign = 1024;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Workspace {
-  float* resid;
-  void* xb;          // bf16(residual) = A operand of QKV / gate-up (norm applied in epilogue)
+  // residual stream x = hi + lo as a bf16 pair: hi = bf16(x) is the A operand of the QKV and
+  // gate/up GEMMs (their epilogues apply the fused RMSNorm), lo = bf16(x - hi)
+  void* xb;          // hi
+  void* rlo;         // lo
   float* ss_attn;    // per-row sum of squares of the residual feeding the attention block
   float* ss_mlp;     // ... feeding the MLP block
   void* qkv;
   void* attn;
   void* hbuf;
   void* attn_c;      // [n_items x H*dh] bf16  last-layer compacted rows
-  float* resid_c;    // [n_items x d] fp32
+  void* hi_c;        // [n_items x d] bf16
+  void* lo_c;        // [n_items x d] bf16
   // device copies of host inputs/outputs (pf_score_host)
   int32_t *ids, *pos, *segs, *work, *last_idx;
   float *logits2, *p_yes;
@@ -116,15 +119,16 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   Workspace w{};
   size_t off = 0;
   auto take = [&](size_t bytes) { uint8_t* p = base + off; off = align_up(off + bytes); return p; };
-  w.resid = reinterpret_cast<float*>(take((size_t)T * d.d_model * 4));
   w.xb = take((size_t)T * d.d_model * 2);
+  w.rlo = take((size_t)T * d.d_model * 2);
   w.ss_attn = reinterpret_cast<float*>(take((size_t)T * 4));
   w.ss_mlp = reinterpret_cast<float*>(take((size_t)T * 4));
   w.qkv = take((size_t)T * m->qkv_n * 2);
   w.attn = take((size_t)T * m->attn_k * 2);
   w.hbuf = take((size_t)T * d.d_ff_pad * 2);
   w.attn_c = take((size_t)n_items * m->attn_k * 2);
-  w.resid_c = reinterpret_cast<float*>(take((size_t)n_items * d.d_model * 4));
+  w.hi_c = take((size_t)n_items * d.d_model * 2);
+  w.lo_c = take((size_t)n_items * d.d_model * 2);
   w.ids = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.pos = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.segs = reinterpret_cast<int32_t*>(take((size_t)n_seg * 16));
@@ -214,7 +218,7 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
   // Fused RMSNorm: the residual-update epilogues keep xb = bf16(resid) and ss = sum(resid^2);
   // the next GEMM scales its accumulator rows by rsqrt(ss/d + eps) (norm gains are folded into
   // w_qkv / w_gu by the caller, include/prefill_sm100.h).
-  int rc = launch_embed(ids, d.embedding, w.resid, w.xb, w.ss_attn, T, d.d_model, st);
+  int rc = launch_embed(ids, d.embedding, nullptr, w.xb, w.rlo, w.ss_attn, T, d.d_model, st);
   if (rc) return rc;
   for (int l = 0; l < d.n_layers; ++l) {
     GemmDesc g{};
@@ -231,30 +235,30 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     if (l == d.n_layers - 1 && n_items < T && m->last_layer_compact) {
       // Last layer: only the n_items last-token rows reach the head, so the O-projection and MLP
       // run on those rows alone (per-row arithmetic unchanged; tests check bit-equality).
-      if ((rc = launch_gather_rows(last_idx, n_items, w.attn, m->attn_k, w.resid, d.d_model, w.attn_c,
-                                   w.resid_c, st)))
+      if ((rc = launch_gather_rows(last_idx, n_items, w.attn, m->attn_k, w.xb, w.rlo, d.d_model, w.attn_c,
+                                   w.hi_c, w.lo_c, st)))
         return rc;
       GemmDesc o{};
       o.A = w.attn_c; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
-      o.C = w.resid_c; o.ldc = d.d_model; o.M = n_items; o.N = d.d_model; o.K = m->attn_k;
-      o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp;
+      o.C = w.lo_c; o.ldc = d.d_model; o.M = n_items; o.N = d.d_model; o.K = m->attn_k;
+      o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.hi_c; o.ldxb = d.d_model; o.ss_out = w.ss_mlp;
       if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
       GemmDesc gu{};
-      gu.A = w.xb; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
+      gu.A = w.hi_c; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
       gu.C = w.hbuf; gu.ldc = d.d_ff_pad; gu.M = n_items; gu.N = 2 * d.d_ff_pad; gu.K = d.d_model;
-      gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.inv_d = inv_d; gu.eps = eps;
+      gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.ss_zero = w.ss_attn; gu.inv_d = inv_d; gu.eps = eps;
       if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
       GemmDesc dn{};
       dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
-      dn.C = w.resid_c; dn.ldc = d.d_model; dn.M = n_items; dn.N = d.d_model; dn.K = d.d_ff_pad;
-      dn.epilogue = EPI_RESID_ADD;
+      dn.C = w.lo_c; dn.ldc = d.d_model; dn.M = n_items; dn.N = d.d_model; dn.K = d.d_ff_pad;
+      dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.hi_c; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn;
       if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
-      return launch_head(w.resid_c, nullptr, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
-                         logits2, p_yes, bad, st);
+      return launch_head(nullptr, w.hi_c, w.lo_c, nullptr, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no,
+                         eps, logits2, p_yes, bad, st);
     }
     GemmDesc o{};
     o.A = w.attn; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
-    o.C = w.resid; o.ldc = d.d_model; o.M = T; o.N = d.d_model; o.K = m->attn_k;
+    o.C = w.rlo; o.ldc = d.d_model; o.M = T; o.N = d.d_model; o.K = m->attn_k;
     o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp;
     if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
     GemmDesc gu{};
@@ -264,11 +268,11 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
     GemmDesc dn{};
     dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
-    dn.C = w.resid; dn.ldc = d.d_model; dn.M = T; dn.N = d.d_model; dn.K = d.d_ff_pad;
+    dn.C = w.rlo; dn.ldc = d.d_model; dn.M = T; dn.N = d.d_model; dn.K = d.d_ff_pad;
     dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.xb; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn;
     if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
   }
-  return launch_head(w.resid, last_idx, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
+  return launch_head(nullptr, w.xb, w.rlo, last_idx, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
                      logits2, p_yes, bad, st);
 }
 
@@ -363,9 +367,9 @@ int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ld
   return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int pf_embed(const int32_t* ids, const void* emb, float* resid, void* xb, float* ss, int T, int d,
+int pf_embed(const int32_t* ids, const void* emb, float* resid, void* hi, void* lo, float* ss, int T, int d,
              pf_stream_t stream) {
-  return launch_embed(ids, emb, resid, xb, ss, T, d, reinterpret_cast<cudaStream_t>(stream));
+  return launch_embed(ids, emb, resid, hi, lo, ss, T, d, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int pf_gemm_bf16_ex(const pf_gemm_args* a, pf_stream_t stream) {
@@ -395,7 +399,7 @@ int pf_prefix_attention(const void* qkv, void* out, int T, int n_heads, int n_kv
 int pf_head_last_token(const float* resid, const int32_t* last_idx, int n_items, int d,
                        const float* g, const float* w_yes, const float* w_no, float eps,
                        float* logits2, float* p_yes, int* bad, pf_stream_t stream) {
-  return launch_head(resid, last_idx, n_items, d, g, w_yes, w_no, eps, logits2, p_yes, bad,
+  return launch_head(resid, nullptr, nullptr, last_idx, n_items, d, g, w_yes, w_no, eps, logits2, p_yes, bad,
                      reinterpret_cast<cudaStream_t>(stream));
 }
 

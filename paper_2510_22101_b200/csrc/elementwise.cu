@@ -21,8 +21,8 @@ PF_DEVICE float warp_sum(float v) {
 // operand of layer 0's QKV GEMM) and ss[t] = sum(x^2) (its fused RMSNorm statistic).
 __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ ids,
                                                     const __nv_bfloat16* __restrict__ emb,
-                                                    float* __restrict__ resid, uint4* __restrict__ xb,
-                                                    float* __restrict__ ss, int T, int d) {
+                                                    float* __restrict__ resid, uint4* __restrict__ hi,
+                                                    uint4* __restrict__ lo, float* __restrict__ ss, int T, int d) {
   pdl_launch_dependents();
   pdl_wait();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -30,17 +30,20 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ 
   if (t >= T) return;
   const int id = __ldg(ids + t);
   const uint4* src = reinterpret_cast<const uint4*>(emb + (size_t)id * d);
-  float4* dst = reinterpret_cast<float4*>(resid + (size_t)t * d);
+  float4* dst = resid ? reinterpret_cast<float4*>(resid + (size_t)t * d) : nullptr;
   float acc = 0.f;
   for (int i = lane; i < d / 8; i += 32) {
     const uint4 u = __ldg(src + i);
     const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
     const float2 a = __bfloat1622float2(p[0]), b = __bfloat1622float2(p[1]);
-    const float2 c = __bfloat1622float2(p[2]), e = __bfloat1622float2(p[3]);
-    dst[2 * i] = make_float4(a.x, a.y, b.x, b.y);
-    dst[2 * i + 1] = make_float4(c.x, c.y, e.x, e.y);
-    if (xb) xb[(size_t)t * (d / 8) + i] = u;
-    acc += a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y + c.x * c.x + c.y * c.y + e.x * e.x + e.y * e.y;
+    const float2 c = __bfloat1622float2(p[2]), f = __bfloat1622float2(p[3]);
+    if (dst) {
+      dst[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+      dst[2 * i + 1] = make_float4(c.x, c.y, f.x, f.y);
+    }
+    if (hi) hi[(size_t)t * (d / 8) + i] = u;                       // embedding rows are bf16: lo = 0
+    if (lo) lo[(size_t)t * (d / 8) + i] = make_uint4(0u, 0u, 0u, 0u);
+    acc += a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y + c.x * c.x + c.y * c.y + f.x * f.x + f.y * f.y;
   }
   if (ss) {
     acc = warp_sum(acc);
@@ -87,6 +90,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 // ---------------------------------------------------------------- last-token head
 // One warp per item: never forms [N x V] logits — only the yes/no columns of W_head are read.
 __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ resid,
+                                                   const __nv_bfloat16* __restrict__ rhi,
+                                                   const __nv_bfloat16* __restrict__ rlo,
                                                    const int32_t* __restrict__ last_idx,
                                                    int n_items, int d,
                                                    const float* __restrict__ g,
@@ -99,14 +104,17 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ res
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n_items) return;
-  const float* x = resid + (size_t)(last_idx ? __ldg(last_idx + i) : i) * d;
+  const size_t r = (size_t)(last_idx ? __ldg(last_idx + i) : i) * d;
+  auto X = [&](int j) -> float {   // residual value: fp32, or the bf16 hi/lo pair
+    return resid ? resid[r + j] : __bfloat162float(rhi[r + j]) + __bfloat162float(rlo[r + j]);
+  };
   float ss = 0.f;
-  for (int j = lane; j < d; j += 32) { const float v = x[j]; ss += v * v; }
+  for (int j = lane; j < d; j += 32) { const float v = X(j); ss += v * v; }
   ss = warp_sum(ss);
-  const float r = rsqrtf(ss / (float)d + eps);
+  const float rs = rsqrtf(ss / (float)d + eps);
   float ly = 0.f, ln = 0.f;
   for (int j = lane; j < d; j += 32) {
-    const float hn = x[j] * r * __ldg(g + j);
+    const float hn = X(j) * rs * __ldg(g + j);
     ly += hn * __ldg(w_yes + j);
     ln += hn * __ldg(w_no + j);
   }
@@ -125,8 +133,9 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ res
 // attn_c[i] = attn[last_idx[i]] (bf16), resid_c[i] = resid[last_idx[i]] (fp32).
 __global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restrict__ last_idx, int n,
                                                           const uint4* __restrict__ attn, int attn_v4,
-                                                          const float4* __restrict__ resid, int resid_v4,
-                                                          uint4* __restrict__ attn_c, float4* __restrict__ resid_c) {
+                                                          const uint4* __restrict__ hi, const uint4* __restrict__ lo,
+                                                          int resid_v4, uint4* __restrict__ attn_c,
+                                                          uint4* __restrict__ hi_c, uint4* __restrict__ lo_c) {
   pdl_launch_dependents();
   pdl_wait();
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -134,25 +143,30 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restr
   if (i >= n) return;
   const size_t r = (size_t)__ldg(last_idx + i);
   for (int j = lane; j < attn_v4; j += 32) attn_c[(size_t)i * attn_v4 + j] = __ldg(attn + r * attn_v4 + j);
-  for (int j = lane; j < resid_v4; j += 32) resid_c[(size_t)i * resid_v4 + j] = __ldg(resid + r * resid_v4 + j);
+  for (int j = lane; j < resid_v4; j += 32) {
+    hi_c[(size_t)i * resid_v4 + j] = __ldg(hi + r * resid_v4 + j);
+    lo_c[(size_t)i * resid_v4 + j] = __ldg(lo + r * resid_v4 + j);
+  }
 }
 
-int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const float* resid,
-                       int d, void* attn_c, float* resid_c, cudaStream_t stream) {
+int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const void* hi,
+                       const void* lo, int d, void* attn_c, void* hi_c, void* lo_c, cudaStream_t stream) {
   if (n == 0) return 0;
   gather_rows_kernel<<<(n + 7) / 8, 256, 0, stream>>>(
-      last_idx, n, reinterpret_cast<const uint4*>(attn), attn_cols / 8, reinterpret_cast<const float4*>(resid),
-      d / 4, reinterpret_cast<uint4*>(attn_c), reinterpret_cast<float4*>(resid_c));
+      last_idx, n, reinterpret_cast<const uint4*>(attn), attn_cols / 8, reinterpret_cast<const uint4*>(hi),
+      reinterpret_cast<const uint4*>(lo), d / 8, reinterpret_cast<uint4*>(attn_c), reinterpret_cast<uint4*>(hi_c),
+      reinterpret_cast<uint4*>(lo_c));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "gather launch: %s", cudaGetErrorString(e));
 }
 
-int launch_embed(const int32_t* ids, const void* emb, float* resid, void* xb, float* ss, int T, int d,
-                 cudaStream_t stream) {
+int launch_embed(const int32_t* ids, const void* emb, float* resid, void* hi, void* lo, float* ss, int T,
+                 int d, cudaStream_t stream) {
   if (d % 8 != 0) return fail(-2, "embed: d_model must be a multiple of 8");
   if (T == 0) return 0;
-  embed_kernel<<<(T + 7) / 8, 256, 0, stream>>>(ids, reinterpret_cast<const __nv_bfloat16*>(emb),
-                                                resid, reinterpret_cast<uint4*>(xb), ss, T, d);
+  embed_kernel<<<(T + 7) / 8, 256, 0, stream>>>(ids, reinterpret_cast<const __nv_bfloat16*>(emb), resid,
+                                                reinterpret_cast<uint4*>(hi), reinterpret_cast<uint4*>(lo), ss,
+                                                T, d);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "embed launch: %s", cudaGetErrorString(e));
 }
@@ -176,12 +190,13 @@ int launch_rmsnorm(const float* x, const float* g, void* y, int T, int d, float 
   return e == cudaSuccess ? 0 : fail(-4, "rmsnorm launch: %s", cudaGetErrorString(e));
 }
 
-int launch_head(const float* resid, const int32_t* last_idx, int n_items, int d,
-                const float* g, const float* w_yes, const float* w_no, float eps, float* logits2,
+int launch_head(const float* resid, const void* rhi, const void* rlo, const int32_t* last_idx, int n_items,
+                int d, const float* g, const float* w_yes, const float* w_no, float eps, float* logits2,
                 float* p_yes, int* bad, cudaStream_t stream) {
   if (n_items == 0) return 0;
-  head_kernel<<<(n_items + 7) / 8, 256, 0, stream>>>(resid, last_idx, n_items, d, g, w_yes, w_no,
-                                                     eps, logits2, p_yes, bad);
+  head_kernel<<<(n_items + 7) / 8, 256, 0, stream>>>(resid, reinterpret_cast<const __nv_bfloat16*>(rhi),
+                                                     reinterpret_cast<const __nv_bfloat16*>(rlo), last_idx,
+                                                     n_items, d, g, w_yes, w_no, eps, logits2, p_yes, bad);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "head launch: %s", cudaGetErrorString(e));
 }

@@ -31,9 +31,11 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 // CG = CTAs per MMA (cta_group).  CG=2: a CTA pair computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 (M=256); each CTA loads its own 128 A rows and half (128) of the
 // B rows, so per-CTA operand bytes per MMA drop from 48 KB to 32 KB per k-block.
-// EPI_RESID_ADD_NORM reads the old residual through a per-warp ring of RB_DEPTH TMA-loaded
+// EPI_RESID_ADD_NORM reads the old residual (bf16 hi/lo pair) through a per-warp ring of
+// RB_DEPTH TMA-loaded 64-column chunks (hi box + lo box, 8 KB), updating it in place.
 // 32x32 fp32 chunks (4 KB each), so it trades two mainloop stages for that ring.
-constexpr int RB_DEPTH = 4;
+constexpr int RB_DEPTH = 3;
+constexpr int RB_SLOT = 2 * GEMM_STG_BYTES;           // hi + lo boxes of one 64-column chunk
 template <int CG, int EPI>
 struct GemmCfg {
   static constexpr int B_ROWS = GEMM_BN / CG;                // B rows loaded per CTA
@@ -41,8 +43,8 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
   static constexpr bool RING = EPI == EPI_RESID_ADD_NORM;
   static constexpr int STAGES = RING ? 4 : (CG == 2 ? 6 : 4);
-  // ring: RB_DEPTH fp32 chunk buffers + 2 bf16 staging boxes per epilogue warp
-  static constexpr int EPI_BYTES = RING ? 4 * (RB_DEPTH + 2) * GEMM_STG_BYTES : 4 * 2 * GEMM_STG_BYTES;
+  // ring: RB_DEPTH (hi, lo) chunk slots per epilogue warp; otherwise 2 staging boxes per warp
+  static constexpr int EPI_BYTES = RING ? 4 * RB_DEPTH * RB_SLOT : 4 * 2 * GEMM_STG_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
   static constexpr int TILE_M = GEMM_BM * CG;
 };
@@ -241,17 +243,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---- EPI_RESID_ADD_NORM residual ring: chunk k of this warp lives in buffer k % RB_DEPTH
     uint64_t* my_rbar = rbar + (warp - 2) * RB_DEPTH;
     uint32_t ring_issued = 0, ring_used = 0;
-    auto ring_issue = [&](int t, int c) {   // TMA-load chunk c (32 cols) of tile t's 32 rows
+    auto ring_issue = [&](int t, int c) {   // TMA-load chunk c (64 cols, hi + lo) of tile t's 32 rows
       const int mm = (t / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM + quad * 32;
-      const int nn = (t % args.num_n_blk) * GEMM_BN + c * 32;
+      const int nn = (t % args.num_n_blk) * GEMM_BN + c * 64;
       const uint32_t b = ring_issued % RB_DEPTH;
       if (lane == 0) {
-        mbar_arrive_expect_tx(&my_rbar[b], GEMM_STG_BYTES);
-        tma_load_2d(my_stg + b * GEMM_STG_BYTES, &tmC, &my_rbar[b], nn, mm, kEvictFirst);
+        mbar_arrive_expect_tx(&my_rbar[b], RB_SLOT);
+        tma_load_2d(my_stg + b * RB_SLOT, &tmD, &my_rbar[b], nn, mm, kEvictFirst);                    // hi
+        tma_load_2d(my_stg + b * RB_SLOT + GEMM_STG_BYTES, &tmC, &my_rbar[b], nn, mm, kEvictFirst);   // lo
       }
       ++ring_issued;
     };
-    auto ring_chunks = [&](int t) { return min(GEMM_BN / 32, (args.N - (t % args.num_n_blk) * GEMM_BN) / 32); };
+    auto ring_chunks = [&](int t) { return min(GEMM_BN / 64, (args.N - (t % args.num_n_blk) * GEMM_BN) / 64); };
     if constexpr (Cfg::RING) {
       if (grp < num_tiles)
         for (int c = 0; c < min(RB_DEPTH, ring_chunks(grp)); ++c) ring_issue(grp, c);
@@ -293,64 +296,62 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           emit(v, n0 + c * 32, r0);
         }
       } else if constexpr (EPI == EPI_RESID_ADD_NORM) {
-        // new = old + acc (fp32) -> resid;  bf16(new) -> xb (next GEMM's A operand);
-        // ss_out[row] += sum(new^2) (next RMSNorm).  Old residual chunks arrive by TMA into a
-        // per-warp ring (the first RB_DEPTH issued while this tile's MMAs ran); the new values
-        // overwrite the chunk in place and leave by TMA store, the bf16 copy through a 64-column
-        // staging box.  Bulk-group accounting: iteration k commits G_f(k) and, for odd k, G_b(k).
+        // Residual stream as a bf16 pair: x = hi + lo, hi = bf16(x) (the next GEMM's A operand),
+        // lo = bf16(x - hi) (~16 mantissa bits together).  new = hi + lo + acc in fp32; hi/lo are
+        // rewritten in place in the ring slot and leave by TMA store; ss_out[row] += sum(new^2)
+        // (next RMSNorm).  Old chunks arrive through the TMA ring (the first RB_DEPTH issued while
+        // this tile's MMAs ran).  Bulk groups: one per chunk (hi + lo stores).
         const int n_chunks = ring_chunks(tile);
-        uint8_t* bf_stg = my_stg + RB_DEPTH * GEMM_STG_BYTES;
         float ssq = 0.f;
 #pragma unroll 1
         for (int c = 0; c < n_chunks; ++c) {
           const uint32_t k = ring_used;
           const uint32_t b = k % RB_DEPTH;
-          // G_f(k-2) has exactly two later groups: once it has been read, chunk k-2's buffer can be
-          // refilled and (for even c) the bf16 box last stored as G_b(k-3) can be rewritten.
+          // G(k-2) has exactly one later group: once read, its slot takes chunk c + RB_DEPTH - 2
           if (c >= 2) {
-            if (lane == 0) tma_store_wait_read<2>();
+            if (lane == 0) tma_store_wait_read<1>();
             __syncwarp();
-            if (c + 2 < n_chunks) ring_issue(tile, c + 2);
+            if (c + RB_DEPTH - 2 < n_chunks) ring_issue(tile, c + RB_DEPTH - 2);
           }
           mbar_wait(&my_rbar[b], (k / RB_DEPTH) & 1);
           ++ring_used;
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c * 32, v);
-          const uint32_t rrow = smem_u32(my_stg + b * GEMM_STG_BYTES) + lane * 128;
-          const uint32_t brow = smem_u32(bf_stg + ((c >> 1) & 1) * GEMM_STG_BYTES) + lane * 128;
+          uint32_t v0[32], v1[32];
+          tmem_ld_32x32b_x32(t_row + c * 64, v0);
+          tmem_ld_32x32b_x32(t_row + c * 64 + 32, v1);
+          const uint32_t hrow = smem_u32(my_stg + b * RB_SLOT) + lane * 128;
+          const uint32_t lrow = hrow + GEMM_STG_BYTES;
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t addr = rrow + ((j ^ (lane & 7)) << 4);
-            float4 o;
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w) : "r"(addr));
-            o.x += __uint_as_float(v[4 * j]);
-            o.y += __uint_as_float(v[4 * j + 1]);
-            o.z += __uint_as_float(v[4 * j + 2]);
-            o.w += __uint_as_float(v[4 * j + 3]);
-            ssq += o.x * o.x + o.y * o.y + o.z * o.z + o.w * o.w;
-            st_shared_v4(addr, __float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z),
-                         __float_as_uint(o.w));
-            const uint32_t p0 = pack_bf16x2(o.x, o.y), p1 = pack_bf16x2(o.z, o.w);
-            // bf16: 32 fp32 cols = 64 B = 16 B chunks [(c&1)*4, (c&1)*4+4) of the 128 B row
-            if (j & 1) {
-              asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(brow + ((((c & 1) * 4 + (j >> 1)) ^ (lane & 7)) << 4) + 8),
-                           "r"(p0), "r"(p1) : "memory");
-            } else {
-              asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(brow + ((((c & 1) * 4 + (j >> 1)) ^ (lane & 7)) << 4)),
-                           "r"(p0), "r"(p1) : "memory");
+          for (int j = 0; j < 8; ++j) {      // 16 B chunk j = columns [8j, 8j+8) of this 64-col chunk
+            const uint32_t off = (j ^ (lane & 7)) << 4;
+            uint32_t h[4], l[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(h[0]), "=r"(h[1]), "=r"(h[2]), "=r"(h[3]) : "r"(hrow + off));
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(l[0]), "=r"(l[1]), "=r"(l[2]), "=r"(l[3]) : "r"(lrow + off));
+            uint32_t nh[4], nl[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int col = 8 * j + 2 * e;      // within the 64-col chunk
+              const float a0 = (col < 32) ? __uint_as_float(v0[col]) : __uint_as_float(v1[col - 32]);
+              const float a1 = (col + 1 < 32) ? __uint_as_float(v0[col + 1]) : __uint_as_float(v1[col + 1 - 32]);
+              const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&h[e]);
+              const __nv_bfloat162 lb = *reinterpret_cast<const __nv_bfloat162*>(&l[e]);
+              const float x0 = __bfloat162float(hb.x) + __bfloat162float(lb.x) + a0;
+              const float x1 = __bfloat162float(hb.y) + __bfloat162float(lb.y) + a1;
+              ssq += x0 * x0 + x1 * x1;
+              const __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+              const __nv_bfloat162 l2 = __floats2bfloat162_rn(x0 - __bfloat162float(h2.x), x1 - __bfloat162float(h2.y));
+              nh[e] = *reinterpret_cast<const uint32_t*>(&h2);
+              nl[e] = *reinterpret_cast<const uint32_t*>(&l2);
             }
+            st_shared_v4(hrow + off, nh[0], nh[1], nh[2], nh[3]);
+            st_shared_v4(lrow + off, nl[0], nl[1], nl[2], nl[3]);
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, my_stg + b * GEMM_STG_BYTES, n0 + c * 32, r0);
+            tma_store_2d(&tmD, my_stg + b * RB_SLOT, n0 + c * 64, r0);
+            tma_store_2d(&tmC, my_stg + b * RB_SLOT + GEMM_STG_BYTES, n0 + c * 64, r0);
             tma_store_commit();
-            if (c & 1) {
-              tma_store_2d(&tmD, bf_stg + ((c >> 1) & 1) * GEMM_STG_BYTES, n0 + (c >> 1) * 64, r0);
-              tma_store_commit();
-            }
           }
         }
         if (rvalid) atomicAdd(args.ss_out + grow, ssq);
@@ -549,7 +550,7 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
   if (cached_b) tb = *cached_b;
   else if (!make_weight_tmap(&tb, d.B, d.N, d.K, d.ldb)) return -3;
   const int out_cols = d.epilogue == EPI_SWIGLU ? d.N / 2 : d.N;
-  if (d.epilogue == EPI_RESID_ADD || d.epilogue == EPI_RESID_ADD_NORM) {
+  if (d.epilogue == EPI_RESID_ADD) {
     if (!make_tmap_2d(&tc, d.C, 4, d.M, out_cols, d.ldc, 32, 32, true)) return -3;
   } else {
     if (!make_tmap_2d(&tc, d.C, 2, d.M, out_cols, d.ldc, 32, 64, true)) return -3;

@@ -12,7 +12,7 @@ enum Epilogue : int {
   EPI_ROPE_BF16 = 1,
   EPI_SWIGLU = 2,
   EPI_RESID_ADD = 3,
-  EPI_RESID_ADD_NORM = 4,   // resid += acc (fp32), xb = bf16(resid), ss_out[row] += sum(resid^2)
+  EPI_RESID_ADD_NORM = 4,   // (hi=xb, lo=C) bf16 pair += acc in place, ss_out[row] += sum(new^2)
 };
 
 // ---- programmatic dependent launch switch (PF_NO_PDL=1 disables)
@@ -59,13 +59,14 @@ int gemm_smem_bytes();
 int gemm_cta_group();   // 2 (default) or 1 via PF_GEMM_CTAS=1
 bool make_weight_tmap(CUtensorMap* out, const void* B, int N, int K, int ldb);
 
-int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, void* xb, float* ss, int T,
+int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, void* hi, void* lo, float* ss, int T,
                  int d, cudaStream_t stream);
 int launch_rmsnorm(const float* resid, const float* gamma, void* out_bf16, int T, int d, float eps,
                    cudaStream_t stream);
-int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const float* resid,
-                       int d, void* attn_c, float* resid_c, cudaStream_t stream);
-int launch_head(const float* resid, const int32_t* last_idx, int n_items, int d,
+int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const void* hi,
+                       const void* lo, int d, void* attn_c, void* hi_c, void* lo_c, cudaStream_t stream);
+// resid (fp32) or, when resid == nullptr, the bf16 (hi, lo) pair
+int launch_head(const float* resid, const void* rhi, const void* rlo, const int32_t* last_idx, int n_items, int d,
                 const float* final_gamma, const float* w_yes, const float* w_no, float eps,
                 float* logits2, float* p_yes, int* bad_flag, cudaStream_t stream);
 

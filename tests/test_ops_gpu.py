@@ -160,11 +160,13 @@ def test_embed_rmsnorm_head(lib):
     ids = torch.randint(0, V, (T,), device="cuda", dtype=torch.int32)
     resid = torch.empty(T, d, device="cuda")
     xb = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    lo = torch.full((T, d), 7.0, device="cuda", dtype=torch.bfloat16)
     ss = torch.empty(T, device="cuda")
-    _lib.check(lib.pf_embed(P(ids), P(emb), P(resid), P(xb), P(ss), T, d, stream()))
+    _lib.check(lib.pf_embed(P(ids), P(emb), P(resid), P(xb), P(lo), P(ss), T, d, stream()))
     torch.cuda.synchronize()
     torch.testing.assert_close(resid, emb[ids.long()].float(), rtol=0, atol=0)
     torch.testing.assert_close(xb, emb[ids.long()], rtol=0, atol=0)
+    assert float(lo.abs().max()) == 0.0
     torch.testing.assert_close(ss, emb[ids.long()].float().pow(2).sum(-1), rtol=1e-5, atol=1e-3)
 
     x = torch.randn(T, d, device="cuda") * 3
@@ -202,20 +204,23 @@ def gemm_ex(lib, **kw):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("M,N,K", [(1000, 256, 128), (5000, 2048, 1280)])
+@pytest.mark.parametrize("M,N,K", [(1000, 256, 128), (5000, 2048, 1280), (700, 384, 256)])
 def test_gemm_resid_add_norm(lib, M, N, K):
-    """Fused RMSNorm producer: C += A.B^T (fp32), xb = bf16(C), ss_out += row sum of squares."""
+    """Fused RMSNorm producer on the bf16 residual pair x = hi + lo: x += A.B^T in place
+    (hi = bf16(x), lo = bf16(x - hi)), ss_out += row sum of squares of the new x."""
     A = rand_bf16(M, K, seed=30)
     B = rand_bf16(N, K, scale=K ** -0.5, seed=31)
-    C0 = torch.randn(M, N, device="cuda")
-    C = C0.clone()
-    xb = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    x0 = torch.randn(M, N, device="cuda") * 4
+    hi = x0.to(torch.bfloat16)
+    lo = (x0 - hi.float()).to(torch.bfloat16)
+    x0 = hi.float() + lo.float()
     ss = torch.full((M,), 0.25, device="cuda")
-    gemm_ex(lib, A=A, lda=K, B=B, ldb=K, C=C, ldc=N, M=M, N=N, K=K, epilogue=_lib.EPI_RESID_ADD_NORM,
-            xb=xb, ldxb=N, ss_out=ss)
-    ref = C0 + A.float() @ B.float().t()
-    torch.testing.assert_close(C, ref, rtol=1e-4, atol=1e-4)
-    torch.testing.assert_close(xb.float(), C.to(torch.bfloat16).float(), rtol=0, atol=0)
+    gemm_ex(lib, A=A, lda=K, B=B, ldb=K, C=lo, ldc=N, M=M, N=N, K=K, epilogue=_lib.EPI_RESID_ADD_NORM,
+            xb=hi, ldxb=N, ss_out=ss)
+    ref = x0 + A.float() @ B.float().t()
+    x = hi.float() + lo.float()
+    torch.testing.assert_close(x, ref, rtol=2e-5, atol=2e-5)          # pair keeps ~16 mantissa bits
+    assert bool(((hi.float() - x).abs() <= x.abs() * 2.0 ** -8 + 1e-30).all())   # hi = bf16(x), half-ulp
     torch.testing.assert_close(ss, 0.25 + ref.pow(2).sum(-1), rtol=1e-4, atol=1e-2)
 
 

@@ -14,7 +14,7 @@ for n, M, N, K, epi, _ in gb.SHAPES:
     A = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
     B = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
     ncol = N // 2 if epi == _lib.EPI_SWIGLU else N
-    C = torch.zeros(M, ncol, device="cuda", dtype=torch.float32 if epi in (3, 4) else torch.bfloat16)
+    C = torch.zeros(M, ncol, device="cuda", dtype=torch.float32 if epi == 3 else torch.bfloat16)
     xb = torch.empty(M, ncol, device="cuda", dtype=torch.bfloat16)
     ss = torch.ones(M, device="cuda")
     pos = torch.zeros(M, device="cuda", dtype=torch.int32)
