@@ -75,7 +75,8 @@ PF_DEVICE float4 ldg_cg_f4(const float* p) {
   return v;
 }
 
-PF_DEVICE float silu(float g) { return g / (1.0f + __expf(-g)); }
+// silu(g) = g * sigmoid(g) with MUFU ex2/rcp (fast-math; the result is rounded to bf16 anyway)
+PF_DEVICE float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Write 32 packed words (one 128-byte row) into a 32x128B swizzled staging box.
 PF_DEVICE void stage_row_128B(uint32_t stg, uint32_t row, const uint32_t (&w)[32]) {
@@ -363,24 +364,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int c = 0; c < min(RB_DEPTH, ring_chunks(nt)); ++c) ring_issue(nt, c);
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
-        // B tile rows [0,128) = gate neurons, [128,256) = matching up neurons.
+        // B tile rows [0,128) = gate neurons, [128,256) = matching up neurons.  The four 32-column
+        // halves are software-pipelined: the next half's tcgen05.ld is in flight during this half's
+        // math (TMEM -> registers is asynchronous until tcgen05.wait::ld).
+        uint32_t gA[32], uA[32], gB[32], uB[32], w[32];
+        tmem_ld_32x32b_x32(t_row, gA);
+        tmem_ld_32x32b_x32(t_row + 128, uA);
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t w[32];
+        for (int cq = 0; cq < 2; ++cq) {       // output chunk cq = cols [64cq, 64cq+64)
+          tmem_ld_wait();
+          tmem_ld_32x32b_x32(t_row + cq * 64 + 32, gB);
+          tmem_ld_32x32b_x32(t_row + 128 + cq * 64 + 32, uB);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t g[32], u[32];
-            tmem_ld_32x32b_x32(t_row + c * 64 + h * 32, g);
-            tmem_ld_32x32b_x32(t_row + 128 + c * 64 + h * 32, u);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float a0 = silu(__uint_as_float(g[2 * i]) * rs) * (__uint_as_float(u[2 * i]) * rs);
-              float a1 = silu(__uint_as_float(g[2 * i + 1]) * rs) * (__uint_as_float(u[2 * i + 1]) * rs);
-              w[h * 16 + i] = pack_bf16x2(a0, a1);
-            }
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = silu(__uint_as_float(gA[2 * i]) * rs) * (__uint_as_float(uA[2 * i]) * rs);
+            const float a1 = silu(__uint_as_float(gA[2 * i + 1]) * rs) * (__uint_as_float(uA[2 * i + 1]) * rs);
+            w[i] = pack_bf16x2(a0, a1);
           }
-          emit(w, n0 / 2 + c * 64, r0);
+          tmem_ld_wait();
+          if (cq == 0) {
+            tmem_ld_32x32b_x32(t_row + 64, gA);
+            tmem_ld_32x32b_x32(t_row + 128 + 64, uA);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = silu(__uint_as_float(gB[2 * i]) * rs) * (__uint_as_float(uB[2 * i]) * rs);
+            const float a1 = silu(__uint_as_float(gB[2 * i + 1]) * rs) * (__uint_as_float(uB[2 * i + 1]) * rs);
+            w[16 + i] = pack_bf16x2(a0, a1);
+          }
+          emit(w, n0 / 2 + cq * 64, r0);
         }
       } else {  // EPI_ROPE_BF16
         // Rotate-half RoPE on heads of width dh (64 or 128): head column e pairs with e + dh/2.

@@ -16,7 +16,12 @@ import torch  # noqa: E402
 from paper_2510_22101_b200 import _lib  # noqa: E402
 
 T = 25664
+T2 = 32832
 SHAPES = [  # name, M, N (B rows), K, epilogue, useful flops (true widths)
+    ("C2 qkv+rope", T2, 4096, 1024, _lib.EPI_ROPE_BF16, 2 * T2 * 4096 * 1024),
+    ("C2 gate/up+swiglu", T2, 6144, 1024, _lib.EPI_SWIGLU, 2 * T2 * 1024 * 6144),
+    ("C2 gate/up plain", T2, 6144, 1024, _lib.EPI_BF16, 2 * T2 * 1024 * 6144),
+    ("C2 o+resid+norm", T2, 1024, 2048, _lib.EPI_RESID_ADD_NORM, 2 * T2 * 1024 * 2048),
     ("qkv+rope", T, 2560, 2048, _lib.EPI_ROPE_BF16, 2 * T * 2560 * 2048),
     ("o+resid", T, 2048, 1280, _lib.EPI_RESID_ADD, 2 * T * 2048 * 1280),
     ("gate/up+swiglu", T, 7424, 2048, _lib.EPI_SWIGLU, 2 * T * 2048 * 2 * 3686),
@@ -48,7 +53,7 @@ def main():
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     cos = torch.rand(2048, 64, device="cuda")
     sin = torch.rand(2048, 64, device="cuda")
-    pos = torch.randint(0, 2048, (T,), device="cuda", dtype=torch.int32)
+    pos = torch.randint(0, 2048, (max(T, T2),), device="cuda", dtype=torch.int32)
     res = []
     for name, M, N, K, epi, flops in SHAPES:
         A = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
@@ -60,7 +65,7 @@ def main():
         ss = torch.ones(M, device="cuda")
         args = _lib.PfGemmArgs(A=A.data_ptr(), lda=K, B=B.data_ptr(), ldb=K, C=C.data_ptr(), ldc=ncol, M=M, N=N,
                                K=K, epilogue=epi, pos=pos.data_ptr() if epi == 1 else None,
-                               rope_cos=cos.data_ptr(), rope_sin=sin.data_ptr(), rope_heads=15 if epi == 1 else 0,
+                               rope_cos=cos.data_ptr(), rope_sin=sin.data_ptr(), rope_heads=(N // 128) * 3 // 4 if epi == 1 else 0,
                                row_ss=ss.data_ptr() if epi in (1, 2) else None,
                                ss_out=ss.data_ptr() if xb is not None else None,
                                xb=xb.data_ptr() if xb is not None else None, ldxb=ncol, inv_d=1.0 / K, eps=1e-6)
