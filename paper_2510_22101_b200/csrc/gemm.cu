@@ -32,9 +32,18 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 // tcgen05.mma.cta_group::2 (M=256); each CTA loads its own 128 A rows and half (128) of the
 // B rows, so per-CTA operand bytes per MMA drop from 48 KB to 32 KB per k-block.
 // EPI_RESID_ADD_NORM reads the old residual (bf16 hi/lo pair) through a per-warp ring of
-// RB_DEPTH TMA-loaded 64-column chunks (hi box + lo box, 8 KB), updating it in place.
-// 32x32 fp32 chunks (4 KB each), so it trades two mainloop stages for that ring.
-constexpr int RB_DEPTH = 3;
+// RB_DEPTH TMA-loaded 64-column chunks (hi box + lo box, 8 KB), updating it in place; it trades
+// mainloop stages for that ring (PF_RING_STAGES / PF_RB_DEPTH override for A/B builds).  5 stages +
+// depth 2 beat 4 + 3 by 2-8 us at the C4 shapes (tools/epi_sweep.py, profiles/r01/epi_sweep.txt):
+// the epilogue math is free (hidden under the MMAs); its 8 B/elem of residual traffic is not, it
+// competes with the mainloop's operand loads in L2 / HBM (~+20 us per GEMM each).
+#ifndef PF_RB_DEPTH
+#define PF_RB_DEPTH 2
+#endif
+#ifndef PF_RING_STAGES
+#define PF_RING_STAGES 5
+#endif
+constexpr int RB_DEPTH = PF_RB_DEPTH;
 constexpr int RB_SLOT = 2 * GEMM_STG_BYTES;           // hi + lo boxes of one 64-column chunk
 template <int CG, int EPI>
 struct GemmCfg {
@@ -42,7 +51,7 @@ struct GemmCfg {
   static constexpr int B_BYTES = B_ROWS * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
   static constexpr bool RING = EPI == EPI_RESID_ADD_NORM;
-  static constexpr int STAGES = RING ? 4 : (CG == 2 ? 6 : 4);
+  static constexpr int STAGES = RING ? PF_RING_STAGES : (CG == 2 ? 6 : 4);
   // ring: RB_DEPTH (hi, lo) chunk slots per epilogue warp; otherwise 2 staging boxes per warp
   static constexpr int EPI_BYTES = RING ? 4 * RB_DEPTH * RB_SLOT : 4 * 2 * GEMM_STG_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
@@ -256,9 +265,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       ++ring_issued;
     };
     auto ring_chunks = [&](int t) { return min(GEMM_BN / 64, (args.N - (t % args.num_n_blk) * GEMM_BN) / 64); };
+    // tile t's first RB_DEPTH chunks go straight into the ring (issued while its MMAs run).  An
+    // extra L2 prefetch of the remaining chunks was measured to make no difference.
+    auto ring_start = [&](int t) {
+      for (int c = 0; c < min(RB_DEPTH, ring_chunks(t)); ++c) ring_issue(t, c);
+    };
     if constexpr (Cfg::RING) {
-      if (grp < num_tiles)
-        for (int c = 0; c < min(RB_DEPTH, ring_chunks(grp)); ++c) ring_issue(grp, c);
+      if (grp < num_tiles) ring_start(grp);
     }
     for (int tile = grp; tile < num_tiles; tile += ngrp) {
       const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
@@ -361,7 +374,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (nt < num_tiles) {
           if (lane == 0) tma_store_wait_read<0>();
           __syncwarp();
-          for (int c = 0; c < min(RB_DEPTH, ring_chunks(nt)); ++c) ring_issue(nt, c);
+          ring_start(nt);
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
         // B tile rows [0,128) = gate neurons, [128,256) = matching up neurons.  The four 32-column
@@ -459,8 +472,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       __syncwarp();
       if (lane == 0) {
         // the MMA issuer waits on the leader CTA's tmem-empty barrier
-        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
-        else mbar_arrive(&tempty_bar[acc]);
+        if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+        else mbar_arrive_relaxed(&tempty_bar[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }

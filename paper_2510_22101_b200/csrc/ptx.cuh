@@ -107,6 +107,13 @@ PF_DEVICE void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar
       : "memory");
 }
 
+// TMA prefetch of one box into L2 (no smem destination, no completion signal).
+PF_DEVICE void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
 PF_DEVICE void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -252,6 +259,16 @@ PF_DEVICE uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 }
 PF_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Relaxed arrives: pure execution signals.  Used where the waiter reads no memory the arriving
+// thread wrote (e.g. "TMEM accumulator drained" after tcgen05.wait::ld + fence::before_thread_sync),
+// so the arrive need not wait for this thread's outstanding global writes / atomics (the release
+// form lowers to MEMBAR.GPU + ERRBAR, a full round trip per tile).
+PF_DEVICE void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+PF_DEVICE void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // TMA load into this CTA's smem whose completion is signalled on the pair leader's mbarrier.
 PF_DEVICE void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar, int32_t c0,

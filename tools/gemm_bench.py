@@ -7,6 +7,7 @@ import argparse
 import ctypes
 import json
 import os
+import re
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -23,6 +24,9 @@ SHAPES = [  # name, M, N (B rows), K, epilogue, useful flops (true widths)
     ("C2 gate/up plain", T2, 6144, 1024, _lib.EPI_BF16, 2 * T2 * 1024 * 6144),
     ("C2 o+resid+norm", T2, 1024, 2048, _lib.EPI_RESID_ADD_NORM, 2 * T2 * 1024 * 2048),
     ("qkv+rope", T, 2560, 2048, _lib.EPI_ROPE_BF16, 2 * T * 2560 * 2048),
+    ("qkv plain", T, 2560, 2048, _lib.EPI_BF16, 2 * T * 2560 * 2048),
+    ("o plain", T, 2048, 1280, _lib.EPI_BF16, 2 * T * 2048 * 1280),
+    ("down plain", T, 2048, 3712, _lib.EPI_BF16, 2 * T * 3686 * 2048),
     ("o+resid", T, 2048, 1280, _lib.EPI_RESID_ADD, 2 * T * 2048 * 1280),
     ("gate/up+swiglu", T, 7424, 2048, _lib.EPI_SWIGLU, 2 * T * 2048 * 2 * 3686),
     ("down+resid", T, 2048, 3712, _lib.EPI_RESID_ADD, 2 * T * 3686 * 2048),
@@ -48,6 +52,8 @@ def time_it(fn, reps=20):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--json", default=None)
+    ap.add_argument("--only", default=None, help="regex on shape names")
+    ap.add_argument("--no-cublas", action="store_true")
     a = ap.parse_args()
     lib = _lib.load()
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -56,6 +62,8 @@ def main():
     pos = torch.randint(0, 2048, (max(T, T2),), device="cuda", dtype=torch.int32)
     res = []
     for name, M, N, K, epi, flops in SHAPES:
+        if a.only and not re.search(a.only, name):
+            continue
         A = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
         B = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
         ncol = N // 2 if epi == _lib.EPI_SWIGLU else N
@@ -75,7 +83,8 @@ def main():
 
         Cb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         cublas = lambda: torch.matmul(A, B.t(), out=Cb)
-        t_ours, t_cub = time_it(ours), time_it(cublas)
+        t_ours = time_it(ours)
+        t_cub = float("nan") if a.no_cublas else time_it(cublas)
         mm_flops = 2.0 * M * N * K
         r = {"name": name, "M": M, "N": N, "K": K, "ours_us": t_ours * 1e3, "cublas_us": t_cub * 1e3,
              "ours_tflops_useful": flops / t_ours / 1e9, "ours_tflops_issued": mm_flops / t_ours / 1e9,

@@ -1,4 +1,4 @@
-"""Top SASS instructions by warp-stall samples for one kernel of an ncu report (needs -lineinfo
+r"""Top SASS instructions by warp-stall samples for one kernel of an ncu report (needs -lineinfo
 and --import-source on).    python tools/ncu_source_hot.py report.ncu-rep 'gemm_bf16_kernel<\(int\)2' [N]"""
 import csv
 import io
