@@ -409,61 +409,83 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       } else {  // EPI_ROPE_BF16
         // Rotate-half RoPE on heads of width dh (64 or 128): head column e pairs with e + dh/2.
-        // For each 32-column block c of the first half the thread loads x1 = cols [32c, 32c+32)
-        // and x2 = cols [dh/2 + 32c, ...); outputs land in 64-column SW128 boxes (dh/64 per head).
+        // Work item i = (head hd, 32-column block c of the first half): x1 = cols [32c, 32c+32),
+        // x2 = cols [dh/2 + 32c, ...).  Items are software-pipelined: item i+1's tcgen05.ld is in
+        // flight during item i's math, cos/sin loads are issued before the TMEM wait, and the wait
+        // for the staging buffer (previous head's TMA store) comes after the math.  Outputs land in
+        // 64-column SW128 boxes: dh=128 -> 2 boxes per head (single-buffered), dh=64 -> 1 box per
+        // head (double-buffered across heads).
         const int dh = args.rope_dh;
         const int half = dh / 2;
+        const int cpb = half / 32;                    // 32-col blocks per head half (1 or 2)
+        const int n_items = GEMM_BN / 32 / 2;         // 4 for both head widths
         const int p = rvalid ? __ldg(args.pos + grow) : 0;
         const float4* cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * half);
         const float4* sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
         const uint32_t stg0 = smem_u32(my_stg);
+        uint32_t x1[32], x2[32];
+        tmem_ld_32x32b_x32(t_row, x1);
+        tmem_ld_32x32b_x32(t_row + half, x2);
 #pragma unroll 1
-        for (int hd = 0; hd < GEMM_BN / dh; ++hd) {
+        for (int it = 0; it < n_items; ++it) {
+          const int hd = it / cpb, c = it % cpb;
           const bool rot = ((n0 + hd * dh) / dh) < args.rope_heads;
-          if (lane == 0) tma_store_wait_read<0>();
-          __syncwarp();
-#pragma unroll 1
-          for (int c = 0; c < half / 32; ++c) {
-            uint32_t x1[32], x2[32];
-            tmem_ld_32x32b_x32(t_row + hd * dh + c * 32, x1);
-            tmem_ld_32x32b_x32(t_row + hd * dh + half + c * 32, x2);
-            tmem_ld_wait();
-            uint32_t w1[16], w2[16];
+          float4 cv[8], sv[8];
 #pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
-              float4 cv = make_float4(1.f, 1.f, 1.f, 1.f), sv = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (rot) { cv = __ldg(cs4 + c * 8 + j4); sv = __ldg(sn4 + c * 8 + j4); }
-              const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
-              const float ss[4] = {sv.x, sv.y, sv.z, sv.w};
-              float o1[4], o2[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float a = __uint_as_float(x1[j4 * 4 + e]) * rs;
-                const float b = __uint_as_float(x2[j4 * 4 + e]) * rs;
-                o1[e] = a * cc[e] - b * ss[e];
-                o2[e] = b * cc[e] + a * ss[e];
-              }
-              w1[j4 * 2] = pack_bf16x2(o1[0], o1[1]);
-              w1[j4 * 2 + 1] = pack_bf16x2(o1[2], o1[3]);
-              w2[j4 * 2] = pack_bf16x2(o2[0], o2[1]);
-              w2[j4 * 2 + 1] = pack_bf16x2(o2[2], o2[3]);
-            }
-            const int e1 = c * 32, e2 = half + c * 32;   // head-local first column of each part
-            const uint32_t b1 = stg0 + (e1 / 64) * GEMM_STG_BYTES + lane * 128;
-            const uint32_t b2 = stg0 + (e2 / 64) * GEMM_STG_BYTES + lane * 128;
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const uint32_t k1 = (e1 % 64) / 8 + q4, k2 = (e2 % 64) / 8 + q4;
-              st_shared_v4(b1 + ((k1 ^ (lane & 7)) << 4), w1[4 * q4], w1[4 * q4 + 1], w1[4 * q4 + 2], w1[4 * q4 + 3]);
-              st_shared_v4(b2 + ((k2 ^ (lane & 7)) << 4), w2[4 * q4], w2[4 * q4 + 1], w2[4 * q4 + 2], w2[4 * q4 + 3]);
-            }
+          for (int j4 = 0; j4 < 8; ++j4) {
+            cv[j4] = rot ? __ldg(cs4 + c * 8 + j4) : make_float4(1.f, 1.f, 1.f, 1.f);
+            sv[j4] = rot ? __ldg(sn4 + c * 8 + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            for (int x = 0; x < dh / 64; ++x)
-              tma_store_2d(&tmC, my_stg + x * GEMM_STG_BYTES, n0 + hd * dh + 64 * x, r0);
-            tma_store_commit();
+          tmem_ld_wait();
+          uint32_t w1[16], w2[16];
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float cc[4] = {cv[j4].x, cv[j4].y, cv[j4].z, cv[j4].w};
+            const float ss[4] = {sv[j4].x, sv[j4].y, sv[j4].z, sv[j4].w};
+            float o1[4], o2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a = __uint_as_float(x1[j4 * 4 + e]) * rs;
+              const float b = __uint_as_float(x2[j4 * 4 + e]) * rs;
+              o1[e] = a * cc[e] - b * ss[e];
+              o2[e] = b * cc[e] + a * ss[e];
+            }
+            w1[j4 * 2] = pack_bf16x2(o1[0], o1[1]);
+            w1[j4 * 2 + 1] = pack_bf16x2(o1[2], o1[3]);
+            w2[j4 * 2] = pack_bf16x2(o2[0], o2[1]);
+            w2[j4 * 2 + 1] = pack_bf16x2(o2[2], o2[3]);
+          }
+          if (it + 1 < n_items) {
+            const int hn = (it + 1) / cpb, cn = (it + 1) % cpb;
+            tmem_ld_32x32b_x32(t_row + hn * dh + cn * 32, x1);
+            tmem_ld_32x32b_x32(t_row + hn * dh + half + cn * 32, x2);
+          }
+          // staging boxes of this head: dh=128 -> boxes {0,1}; dh=64 -> box hd&1
+          const uint32_t hbase = stg0 + (dh == 64 ? (hd & 1) : 0) * GEMM_STG_BYTES;
+          if (c == 0) {
+            if (lane == 0) {
+              if (dh == 64) tma_store_wait_read<1>(); else tma_store_wait_read<0>();
+            }
+            __syncwarp();
+          }
+          const int e1 = c * 32, e2 = half + c * 32;   // head-local first column of each part
+          const uint32_t b1 = hbase + (e1 / 64) * GEMM_STG_BYTES + lane * 128;
+          const uint32_t b2 = hbase + (e2 / 64) * GEMM_STG_BYTES + lane * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint32_t k1 = (e1 % 64) / 8 + q4, k2 = (e2 % 64) / 8 + q4;
+            st_shared_v4(b1 + ((k1 ^ (lane & 7)) << 4), w1[4 * q4], w1[4 * q4 + 1], w1[4 * q4 + 2], w1[4 * q4 + 3]);
+            st_shared_v4(b2 + ((k2 ^ (lane & 7)) << 4), w2[4 * q4], w2[4 * q4 + 1], w2[4 * q4 + 2], w2[4 * q4 + 3]);
+          }
+          if (c == cpb - 1) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const uint8_t* hb = my_stg + (dh == 64 ? (hd & 1) : 0) * GEMM_STG_BYTES;
+              for (int x = 0; x < dh / 64; ++x)
+                tma_store_2d(&tmC, hb + x * GEMM_STG_BYTES, n0 + hd * dh + 64 * x, r0);
+              tma_store_commit();
+            }
           }
         }
       }
