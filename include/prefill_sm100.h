@@ -97,25 +97,49 @@ PF_API int pf_score_host(pf_model* model, const int32_t* ids, const int32_t* pos
                   int n_items, int T, void* workspace, size_t ws_bytes, float* logits2_host,
                   float* p_yes_host, pf_stream_t stream);
 
+/* Calibration capture: the reference forward_prefill's `capture` flag
+ * records each layer's MLP input for the pruning module.
+ * pf_score_capture runs pf_score and, for every layer l, writes
+ *   out[l][i][:] = rmsnorm(x_l[rows[i]]) * gains[l]     (fp32, d_model columns, rows dense)
+ * where x_l is the residual entering layer l's MLP block, for the packed rows `rows`
+ * (device int32[n_rows], each in [0, T)).  gains = the MLP RMSNorm scales [n_layers x d_model]
+ * (fp32, device; the product folds them into w_gu, so capture needs them separately).
+ * Last-layer row compaction is disabled while capturing (every row runs every layer). */
+typedef struct pf_capture {
+  const int32_t* rows;
+  int n_rows;
+  const float* gains;
+  float* out;
+  long long out_layer_stride;   /* elements between out[l] and out[l+1]; 0 = n_rows * d_model */
+} pf_capture;
+
+PF_API int pf_score_capture(pf_model* model, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+                            int n_seg, const int32_t* work, int n_work, const int32_t* last_idx, int n_items,
+                            int T, void* workspace, size_t ws_bytes, float* logits2, float* p_yes,
+                            int* bad_flag, const pf_capture* capture, pf_stream_t stream);
+
 /* Per-op entry points (unit parity tests). */
 /* C = A[MxK] . B[NxK]^T (RoPE heads 128 wide here; pf_gemm_bf16_ex takes rope_dh 64/128)
  * with epilogue 0 bf16, 1 bf16+RoPE, 2 SwiGLU(bf16, N/2 cols),
  * 3 fp32 C += (residual add), 4 residual pair: x = xb + C held as bf16 (hi = xb, lo = C),
- * updated in place to x + acc, and ss_out[row] += sum((x + acc)^2). */
+ * updated in place to x + acc, and ss_out[nb * ss_ld + row] = sum over n-tile nb (256 columns)
+ * of (x + acc)^2 (pf_gemm_bf16_ex). */
 PF_API int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
                  int K, int epilogue, const int32_t* pos, const float* rope_cos,
                  const float* rope_sin, int rope_heads, pf_stream_t stream);
 /* Full-option GEMM (fused RMSNorm): row_ss != NULL scales accumulator row r by
- * rsqrt(row_ss[r] * inv_d + eps); ss_zero rows are cleared by the n-tile-0 CTAs. */
+ * rsqrt(S_r * inv_d + eps), S_r = sum over p < ceil(K/256) of row_ss[p * ss_ld + r] (summed in
+ * order: the forward is bit-reproducible).  ss_ld = row stride of row_ss / ss_out (0 -> M). */
 typedef struct pf_gemm_args {
   const void* A; int lda; const void* B; int ldb; void* C; int ldc;
   int M, N, K, epilogue;
   const int32_t* pos; const float* rope_cos; const float* rope_sin; int rope_heads; int rope_dh;
-  const float* row_ss; float* ss_zero; float* ss_out; void* xb; int ldxb; float inv_d, eps;
+  const float* row_ss; long long ss_ld; float* ss_out; void* xb; int ldxb; float inv_d, eps;
 } pf_gemm_args;
 PF_API int pf_gemm_bf16_ex(const pf_gemm_args* args, pf_stream_t stream);
 /* Embedding gather; every output is optional (NULL skips it): resid = float(E[ids]) (fp32),
- * hi = E[ids] and lo = 0 (the bf16 residual pair the forward keeps), ss = per-row sum of squares. */
+ * hi = E[ids] and lo = 0 (the bf16 residual pair the forward keeps), ss = per-row sum of squares
+ * in the GEMMs' partial layout: ss[t] = sum, ss[p*T + t] = 0 for 1 <= p < ceil(d/256). */
 PF_API int pf_embed(const int32_t* ids, const void* emb, float* resid, void* hi, void* lo, float* ss, int T,
              int d, pf_stream_t stream);
 /* y = bf16(x * rsqrt(mean(x^2) + eps) * gamma); gamma may be NULL (all ones). */

@@ -149,7 +149,7 @@ class KVCache:
         return 0 if not self.k else int(self.k[0].shape[0])
 
 
-def _forward(W: OracleWeights, tokens, prefix: KVCache | None, eps: float):
+def _forward(W: OracleWeights, tokens, prefix: KVCache | None, eps: float, capture: bool = False):
     cfg = W.cfg
     d, H, Hkv, dh, f = dims(cfg)
     dt = W.token_embedding.dtype
@@ -166,6 +166,7 @@ def _forward(W: OracleWeights, tokens, prefix: KVCache | None, eps: float):
     pos = np.arange(P, P + S)
     x = W.token_embedding[tokens].astype(dt)
     cache = KVCache()
+    captured = []
     n_rep = H // Hkv
     for l, lw in enumerate(W.layers):
         h = rmsnorm(x, lw["rms_attn"], eps)
@@ -180,17 +181,22 @@ def _forward(W: OracleWeights, tokens, prefix: KVCache | None, eps: float):
             o = part.output
         x = x + o.transpose(1, 0, 2).reshape(S, H * dh) @ lw["W_o"]
         h2 = rmsnorm(x, lw["rms_mlp"], eps)
+        if capture:
+            captured.append(h2.copy())
         x = x + (silu(h2 @ lw["W_gate"]) * (h2 @ lw["W_up"])) @ lw["W_down"]
         cache.k.append(k)
         cache.v.append(v)
     last = rmsnorm(x[-1:], W.final_norm, eps)[0]
     logits = last @ W.head
+    if capture:
+        return logits, cache, captured
     return logits, cache
 
 
-def forward_prefill(W: OracleWeights, tokens, eps: float = 1e-6):
-    """SPEC.md:200-208 -> (last-token logits [vocab], KVCache)."""
-    return _forward(W, tokens, None, eps)
+def forward_prefill(W: OracleWeights, tokens, eps: float = 1e-6, capture: bool = False):
+    """SPEC.md:200-208 -> (last-token logits [vocab], KVCache); with ``capture`` also the per-layer
+    MLP inputs rmsnorm(x_l) * g_l [S x d] ("capture flag records MLP inputs")."""
+    return _forward(W, tokens, None, eps, capture)
 
 
 def forward_with_prefix(W: OracleWeights, prefix_cache: KVCache, suffix_tokens, eps: float = 1e-6):

@@ -7,6 +7,7 @@ reference spec's names and meanings.
 runs in libprefill_sm100.so (hand-written tcgen05/TMA kernels) behind a C-ABI.
 """
 
+from .calibration import CalibrationSet, capture_calibration, prune_mlp_neurons_calibrated, sample_positions
 from .config import CONFIGS, REQUESTS, ModelConfig, RequestShape
 from .prefixcache import (AttentionPartial, PackedBatch, SharedBatch, merge_attention,
                           pack_requests, pack_token_lists, split_shared_prefix, throughput_gain)
@@ -19,6 +20,7 @@ __all__ = [
     "throughput_gain", "RankedList", "RelevanceScore", "rank_items", "relevance_score", "top_k",
     "DeviceWeights", "Weights", "init_device_weights", "init_weights", "to_device",
     "PrefillScorer", "score_shared_batch",
+    "CalibrationSet", "capture_calibration", "prune_mlp_neurons_calibrated", "sample_positions",
 ]
 
 

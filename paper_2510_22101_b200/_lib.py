@@ -21,7 +21,7 @@ EPI_BF16, EPI_ROPE_BF16, EPI_SWIGLU, EPI_RESID_ADD, EPI_RESID_ADD_NORM = 0, 1, 2
 
 # Every symbol include/prefill_sm100.h declares (tests check the .so exports all of them).
 EXPORTED_SYMBOLS = (
-    "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host",
+    "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host", "pf_score_capture",
     "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
     "pf_last_error", "pf_version", "pf_debug_set_trace",
     "pf_tokenize", "pf_tokenize_spans", "pf_tokenize_batch", "pf_pack_sizes", "pf_pack_requests",
@@ -66,9 +66,15 @@ class PfGemmArgs(ctypes.Structure):
         ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int), ("epilogue", ctypes.c_int),
         ("pos", ctypes.c_void_p), ("rope_cos", ctypes.c_void_p), ("rope_sin", ctypes.c_void_p),
         ("rope_heads", ctypes.c_int), ("rope_dh", ctypes.c_int),
-        ("row_ss", ctypes.c_void_p), ("ss_zero", ctypes.c_void_p), ("ss_out", ctypes.c_void_p),
+        ("row_ss", ctypes.c_void_p), ("ss_ld", ctypes.c_longlong), ("ss_out", ctypes.c_void_p),
         ("xb", ctypes.c_void_p), ("ldxb", ctypes.c_int), ("inv_d", ctypes.c_float), ("eps", ctypes.c_float),
     ]
+
+
+class PfCapture(ctypes.Structure):
+    """include/prefill_sm100.h pf_capture."""
+    _fields_ = [("rows", ctypes.c_void_p), ("n_rows", ctypes.c_int), ("gains", ctypes.c_void_p),
+                ("out", ctypes.c_void_p), ("out_layer_stride", ctypes.c_longlong)]
 
 
 _lib = None
@@ -81,6 +87,8 @@ _SIGS = {
     "pf_model_destroy": (_I, [_P]),
     "pf_workspace_bytes": (ctypes.c_size_t, [_P, _I, _I]),
     "pf_score": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P, _P]),
+    "pf_score_capture": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P,
+                              ctypes.POINTER(PfCapture), _P]),
     "pf_score_host": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P]),
     "pf_gemm_bf16": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),
     "pf_gemm_bf16_ex": (_I, [ctypes.POINTER(PfGemmArgs), _P]),

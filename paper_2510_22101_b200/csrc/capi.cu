@@ -99,8 +99,8 @@ struct Workspace {
   // gate/up GEMMs (their epilogues apply the fused RMSNorm), lo = bf16(x - hi)
   void* xb;          // hi
   void* rlo;         // lo
-  float* ss_attn;    // per-row sum of squares of the residual feeding the attention block
-  float* ss_mlp;     // ... feeding the MLP block
+  float* ss_attn;    // per-row partial sums of squares of the residual feeding the attention block
+  float* ss_mlp;     // ... feeding the MLP block ([ss_parts(d)][T], see pf_internal.h)
   void* qkv;
   void* attn;
   void* hbuf;
@@ -121,8 +121,8 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   auto take = [&](size_t bytes) { uint8_t* p = base + off; off = align_up(off + bytes); return p; };
   w.xb = take((size_t)T * d.d_model * 2);
   w.rlo = take((size_t)T * d.d_model * 2);
-  w.ss_attn = reinterpret_cast<float*>(take((size_t)T * 4));
-  w.ss_mlp = reinterpret_cast<float*>(take((size_t)T * 4));
+  w.ss_attn = reinterpret_cast<float*>(take((size_t)ss_parts(d.d_model) * T * 4));   // [part][T]
+  w.ss_mlp = reinterpret_cast<float*>(take((size_t)ss_parts(d.d_model) * T * 4));
   w.qkv = take((size_t)T * m->qkv_n * 2);
   w.attn = take((size_t)T * m->attn_k * 2);
   w.hbuf = take((size_t)T * d.d_ff_pad * 2);
@@ -210,13 +210,14 @@ size_t pf_workspace_bytes(const pf_model* model, int T, int n_items) {
 static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
                        int n_seg, const int32_t* work, int n_work, const int32_t* last_idx,
                        int n_items, int T, const Workspace& w, float* logits2, float* p_yes,
-                       int* bad, cudaStream_t st) {
+                       int* bad, cudaStream_t st, const pf_capture* cap = nullptr) {
   (void)n_seg;
   const pf_model_desc& d = m->d;
   const float eps = d.rms_eps;
   const float inv_d = 1.0f / (float)d.d_model;
-  // Fused RMSNorm: the residual-update epilogues keep xb = bf16(resid) and ss = sum(resid^2);
-  // the next GEMM scales its accumulator rows by rsqrt(ss/d + eps) (norm gains are folded into
+  // Fused RMSNorm: the residual-update epilogues keep xb = bf16(resid) and ss = sum(resid^2) as
+  // per-n-tile partials; the next GEMM sums them in order and scales its accumulator rows by
+  // rsqrt(ss/d + eps): no atomics, so a pass is bit-reproducible (norm gains are folded into
   // w_qkv / w_gu by the caller, include/prefill_sm100.h).
   int rc = launch_embed(ids, d.embedding, nullptr, w.xb, w.rlo, w.ss_attn, T, d.d_model, st);
   if (rc) return rc;
@@ -226,13 +227,13 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     g.C = w.qkv; g.ldc = m->qkv_n; g.M = T; g.N = m->qkv_n; g.K = d.d_model;
     g.epilogue = EPI_ROPE_BF16; g.pos = pos; g.rope_cos = d.rope_cos; g.rope_sin = d.rope_sin;
     g.rope_heads = d.n_heads + d.n_kv_heads; g.rope_dh = d.d_head; g.max_seq = d.max_seq;
-    g.row_ss = w.ss_attn; g.ss_zero = w.ss_mlp; g.inv_d = inv_d; g.eps = eps;
+    g.row_ss = w.ss_attn; g.ss_ld = T; g.inv_d = inv_d; g.eps = eps;
     if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
     AttnDesc a{};
     a.qkv = w.qkv; a.out = w.attn; a.T = T; a.H = d.n_heads; a.Hkv = d.n_kv_heads; a.dh = d.d_head;
     a.work = work; a.n_work = n_work; a.segs = segs; a.scale = 1.0f / sqrtf((float)d.d_head);
     if ((rc = launch_attention(a, st))) return rc;
-    if (l == d.n_layers - 1 && n_items < T && m->last_layer_compact) {
+    if (l == d.n_layers - 1 && n_items < T && m->last_layer_compact && cap == nullptr) {
       // Last layer: only the n_items last-token rows reach the head, so the O-projection and MLP
       // run on those rows alone (per-row arithmetic unchanged; tests check bit-equality).
       if ((rc = launch_gather_rows(last_idx, n_items, w.attn, m->attn_k, w.xb, w.rlo, d.d_model, w.attn_c,
@@ -241,17 +242,17 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
       GemmDesc o{};
       o.A = w.attn_c; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
       o.C = w.lo_c; o.ldc = d.d_model; o.M = n_items; o.N = d.d_model; o.K = m->attn_k;
-      o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.hi_c; o.ldxb = d.d_model; o.ss_out = w.ss_mlp;
+      o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.hi_c; o.ldxb = d.d_model; o.ss_out = w.ss_mlp; o.ss_ld = T;
       if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
       GemmDesc gu{};
       gu.A = w.hi_c; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
       gu.C = w.hbuf; gu.ldc = d.d_ff_pad; gu.M = n_items; gu.N = 2 * d.d_ff_pad; gu.K = d.d_model;
-      gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.ss_zero = w.ss_attn; gu.inv_d = inv_d; gu.eps = eps;
+      gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.ss_ld = T; gu.inv_d = inv_d; gu.eps = eps;
       if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
       GemmDesc dn{};
       dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
       dn.C = w.lo_c; dn.ldc = d.d_model; dn.M = n_items; dn.N = d.d_model; dn.K = d.d_ff_pad;
-      dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.hi_c; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn;
+      dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.hi_c; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn; dn.ss_ld = T;
       if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
       return launch_head(nullptr, w.hi_c, w.lo_c, nullptr, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no,
                          eps, logits2, p_yes, bad, st);
@@ -259,17 +260,24 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     GemmDesc o{};
     o.A = w.attn; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
     o.C = w.rlo; o.ldc = d.d_model; o.M = T; o.N = d.d_model; o.K = m->attn_k;
-    o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp;
+    o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp; o.ss_ld = T;
     if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
+    if (cap != nullptr &&
+        (rc = launch_capture_rows(cap->rows, cap->n_rows, w.xb, w.rlo, w.ss_mlp, T, cap->gains + (size_t)l * d.d_model,
+                                  d.d_model, eps,
+                                  cap->out + (size_t)l * (cap->out_layer_stride ? (size_t)cap->out_layer_stride
+                                                                                 : (size_t)cap->n_rows * d.d_model),
+                                  st)))
+      return rc;
     GemmDesc gu{};
     gu.A = w.xb; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
     gu.C = w.hbuf; gu.ldc = d.d_ff_pad; gu.M = T; gu.N = 2 * d.d_ff_pad; gu.K = d.d_model;
-    gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.ss_zero = w.ss_attn; gu.inv_d = inv_d; gu.eps = eps;
+    gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.ss_ld = T; gu.inv_d = inv_d; gu.eps = eps;
     if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
     GemmDesc dn{};
     dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
     dn.C = w.rlo; dn.ldc = d.d_model; dn.M = T; dn.N = d.d_model; dn.K = d.d_ff_pad;
-    dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.xb; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn;
+    dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.xb; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn; dn.ss_ld = T;
     if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
   }
   return launch_head(nullptr, w.xb, w.rlo, last_idx, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
@@ -299,6 +307,21 @@ int pf_score(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t*
   Workspace w = layout(m, T, n_items, T, T, static_cast<uint8_t*>(workspace));
   return run_forward(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, w, logits2,
                      p_yes, bad_flag, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_score_capture(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs, int n_seg,
+                     const int32_t* work, int n_work, const int32_t* last_idx, int n_items, int T,
+                     void* workspace, size_t ws_bytes, float* logits2, float* p_yes, int* bad_flag,
+                     const pf_capture* cap, pf_stream_t stream) {
+  size_t need = 0;
+  int rc = check_args(m, T, n_items, n_seg, n_work, workspace, ws_bytes, &need);
+  if (rc) return rc;
+  if (!cap || cap->n_rows < 0 || (cap->n_rows > 0 && (!cap->rows || !cap->gains || !cap->out)) ||
+      (cap->out_layer_stride != 0 && cap->out_layer_stride < (long long)cap->n_rows * m->d.d_model))
+    return fail(-1, "pf_score_capture: bad capture descriptor");
+  Workspace w = layout(m, T, n_items, T, T, static_cast<uint8_t*>(workspace));
+  return run_forward(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, w, logits2, p_yes, bad_flag,
+                     reinterpret_cast<cudaStream_t>(stream), cap);
 }
 
 // Host-side validation of a packed batch (pf_score_host only: the inputs are host memory).
@@ -379,7 +402,7 @@ int pf_gemm_bf16_ex(const pf_gemm_args* a, pf_stream_t stream) {
   g.M = a->M; g.N = a->N; g.K = a->K; g.epilogue = a->epilogue;
   g.pos = a->pos; g.rope_cos = a->rope_cos; g.rope_sin = a->rope_sin; g.rope_heads = a->rope_heads;
   g.rope_dh = a->rope_dh;
-  g.row_ss = a->row_ss; g.ss_zero = a->ss_zero; g.ss_out = a->ss_out; g.xb = a->xb; g.ldxb = a->ldxb;
+  g.row_ss = a->row_ss; g.ss_ld = a->ss_ld; g.ss_out = a->ss_out; g.xb = a->xb; g.ldxb = a->ldxb;
   g.inv_d = a->inv_d; g.eps = a->eps;
   return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -18,7 +18,8 @@ PF_DEVICE float warp_sum(float v) {
 
 // ---------------------------------------------------------------- embedding gather
 // x[t] = float(E[id[t]]) (fp32 residual stream); optionally also xb[t] = E[id[t]] (the bf16 A
-// operand of layer 0's QKV GEMM) and ss[t] = sum(x^2) (its fused RMSNorm statistic).
+// operand of layer 0's QKV GEMM) and ss = sum(x^2) (its fused RMSNorm statistic) in the
+// partial-sum layout the GEMMs read: ss[0*T + t] = sum, ss[p*T + t] = 0 for p = 1..parts-1.
 __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ ids,
                                                     const __nv_bfloat16* __restrict__ emb,
                                                     float* __restrict__ resid, uint4* __restrict__ hi,
@@ -47,7 +48,8 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ 
   }
   if (ss) {
     acc = warp_sum(acc);
-    if (lane == 0) ss[t] = acc;
+    const int parts = ss_parts(d);
+    for (int p = lane; p < parts; p += 32) ss[(size_t)p * T + t] = p == 0 ? acc : 0.f;
   }
 }
 
@@ -158,6 +160,56 @@ int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int att
       reinterpret_cast<uint4*>(lo_c));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "gather launch: %s", cudaGetErrorString(e));
+}
+
+// Calibration capture ("capture flag records MLP inputs for the pruning module"):
+// out[i, :] = rmsnorm(x[rows[i]]) * g, the MLP block's input, for the sampled packed rows.  x is the
+// residual pair hi + lo after the O-projection and ss its per-row partial sums of squares
+// ([ss_parts(d)][ss_ld], summed in order; final once the preceding GEMM completes).  One warp per
+// captured row, 8 columns per lane step.
+__global__ void __launch_bounds__(256) capture_rows_kernel(const int32_t* __restrict__ rows, int n,
+                                                           const uint4* __restrict__ hi,
+                                                           const uint4* __restrict__ lo,
+                                                           const float* __restrict__ ss, int ss_ld,
+                                                           const float* __restrict__ g, int d_v8, float inv_d,
+                                                           float eps, float* __restrict__ out) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const size_t r = (size_t)__ldg(rows + i);
+  float ssum = 0.f;
+  for (int p = 0; p < ss_parts(d_v8 * 8); ++p) ssum += __ldg(ss + (size_t)p * ss_ld + r);
+  const float rs = rsqrtf(ssum * inv_d + eps);
+  float4* o = reinterpret_cast<float4*>(out + (size_t)i * d_v8 * 8);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int j = lane; j < d_v8; j += 32) {
+    const uint4 h = __ldg(hi + r * d_v8 + j), l = __ldg(lo + r * d_v8 + j);
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+    float x[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hw[e]);
+      const __nv_bfloat162 lb = *reinterpret_cast<const __nv_bfloat162*>(&lw[e]);
+      x[2 * e] = __bfloat162float(hb.x) + __bfloat162float(lb.x);
+      x[2 * e + 1] = __bfloat162float(hb.y) + __bfloat162float(lb.y);
+    }
+    const float4 ga = __ldg(g4 + 2 * j), gb = __ldg(g4 + 2 * j + 1);
+    o[2 * j] = make_float4(x[0] * rs * ga.x, x[1] * rs * ga.y, x[2] * rs * ga.z, x[3] * rs * ga.w);
+    o[2 * j + 1] = make_float4(x[4] * rs * gb.x, x[5] * rs * gb.y, x[6] * rs * gb.z, x[7] * rs * gb.w);
+  }
+}
+
+int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* lo, const float* ss, int ss_ld,
+                        const float* g, int d, float eps, float* out, cudaStream_t stream) {
+  if (n == 0) return 0;
+  if (d % 8 != 0) return fail(-2, "capture: d_model must be a multiple of 8");
+  capture_rows_kernel<<<(n + 7) / 8, 256, 0, stream>>>(rows, n, reinterpret_cast<const uint4*>(hi),
+                                                        reinterpret_cast<const uint4*>(lo), ss, ss_ld, g, d / 8,
+                                                        1.0f / (float)d, eps, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "capture launch: %s", cudaGetErrorString(e));
 }
 
 int launch_embed(const int32_t* ids, const void* emb, float* resid, void* hi, void* lo, float* ss, int T,

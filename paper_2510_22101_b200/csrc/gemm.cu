@@ -66,9 +66,10 @@ struct GemmArgs {
   const float* rope_sin;
   int rope_heads;          // heads (of rope_dh cols) that receive RoPE
   int rope_dh;             // head width: 64 or 128
-  const float* row_ss;     // fused RMSNorm: per-row sum of squares of the residual (or null)
-  float* ss_zero;          // rows to clear (n-tile 0) for the next accumulation (or null)
-  float* ss_out;           // EPI_RESID_ADD_NORM: per-row sum of squares accumulator
+  const float* row_ss;     // fused RMSNorm: per-row partial sums of squares [ss_parts_in][ss_ld] (or null)
+  int ss_parts_in;         // = ceil(K / 256): partials written by the producing epilogue
+  int ss_ld;               // row stride of row_ss / ss_out partial arrays
+  float* ss_out;           // EPI_RESID_ADD_NORM: this n-tile's partial sum of squares per row
   const float* resid;      // EPI_RESID_ADD_NORM: residual base pointer (== C)
   int ldr;
   void* xb_out;            // EPI_RESID_ADD_NORM: bf16 copy of the new residual
@@ -284,8 +285,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const bool rvalid = grow < args.M;
       // fused RMSNorm: the A rows were bf16(residual); scale the accumulator row by rstd
       float rs = 1.f;
-      if (args.row_ss != nullptr && rvalid) rs = rsqrtf(__ldg(args.row_ss + grow) * args.inv_d + args.eps);
-      if (args.ss_zero != nullptr && rvalid && (tile % args.num_n_blk) == 0) args.ss_zero[grow] = 0.f;
+      if (args.row_ss != nullptr && rvalid) {
+        // partials summed in a fixed order: bit-reproducible (no atomics anywhere on the path)
+        float ssum = 0.f;
+#pragma unroll 4
+        for (int p = 0; p < args.ss_parts_in; ++p) ssum += __ldg(args.row_ss + (size_t)p * args.ss_ld + grow);
+        rs = rsqrtf(ssum * args.inv_d + args.eps);
+      }
 
       if constexpr (EPI == EPI_BF16) {
 #pragma unroll 1
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       } else if constexpr (EPI == EPI_RESID_ADD_NORM) {
         // Residual stream as a bf16 pair: x = hi + lo, hi = bf16(x) (the next GEMM's A operand),
         // lo = bf16(x - hi) (~16 mantissa bits together).  new = hi + lo + acc in fp32; hi/lo are
-        // rewritten in place in the ring slot and leave by TMA store; ss_out[row] += sum(new^2)
+        // rewritten in place in the ring slot and leave by TMA store; ss_out[nb][row] = sum(new^2)
         // (next RMSNorm).  Old chunks arrive through the TMA ring (the first RB_DEPTH issued while
         // this tile's MMAs ran).  Bulk groups: one per chunk (hi + lo stores).
         const int n_chunks = ring_chunks(tile);
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tma_store_commit();
           }
         }
-        if (rvalid) atomicAdd(args.ss_out + grow, ssq);
+        if (rvalid) args.ss_out[(size_t)(tile % args.num_n_blk) * args.ss_ld + grow] = ssq;
         // start the next tile's residual loads now; they land while its MMAs run
         const int nt = tile + ngrp;
         if (nt < num_tiles) {
@@ -613,7 +619,9 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
   a.num_n_blk = (d.N + GEMM_BN - 1) / GEMM_BN;
   a.pos = d.pos; a.rope_cos = d.rope_cos; a.rope_sin = d.rope_sin; a.rope_heads = d.rope_heads;
   a.rope_dh = d.rope_dh == 64 ? 64 : 128;
-  a.row_ss = d.row_ss; a.ss_zero = d.ss_zero; a.ss_out = d.ss_out;
+  a.row_ss = d.row_ss; a.ss_out = d.ss_out;
+  a.ss_parts_in = ss_parts(d.K);
+  a.ss_ld = d.ss_ld > 0 ? (int)d.ss_ld : d.M;
   a.resid = reinterpret_cast<const float*>(d.C); a.ldr = d.ldc;
   a.xb_out = d.xb; a.ldxb = d.ldxb;
   a.inv_d = d.inv_d; a.eps = d.eps;

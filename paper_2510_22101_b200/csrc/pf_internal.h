@@ -12,7 +12,7 @@ enum Epilogue : int {
   EPI_ROPE_BF16 = 1,
   EPI_SWIGLU = 2,
   EPI_RESID_ADD = 3,
-  EPI_RESID_ADD_NORM = 4,   // (hi=xb, lo=C) bf16 pair += acc in place, ss_out[row] += sum(new^2)
+  EPI_RESID_ADD_NORM = 4,   // (hi=xb, lo=C) bf16 pair += acc in place, ss_out[nb][row] = tile sum(new^2)
 };
 
 // ---- programmatic dependent launch switch (PF_NO_PDL=1 disables)
@@ -45,16 +45,20 @@ struct GemmDesc {
   int rope_dh;     // head width for the RoPE epilogue (64 or 128; 0 -> 128)
   int max_seq;
   // fused RMSNorm (see gemm.cu): A rows are bf16(residual); the epilogue multiplies row r by
-  // rsqrt(row_ss[r]/d + eps).  ss_zero rows are cleared by the n-tile-0 CTAs (for the next
-  // accumulation).  EPI_RESID_ADD_NORM also writes xb (bf16 copy) and accumulates ss_out.
+  // rsqrt(sum_p row_ss[p*ss_ld + r] / d + eps) over the ceil(K/256) partial sums the producing
+  // epilogue stored (fixed order: deterministic).  EPI_RESID_ADD_NORM stores its n-tile nb's
+  // row partial sum(new^2) to ss_out[nb*ss_ld + r] (no atomics).  ss_ld 0 -> M.
   const float* row_ss;
-  float* ss_zero;
+  long long ss_ld;
   float* ss_out;
   void* xb;
   int ldxb;
   float inv_d, eps;
 };
 int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t stream);
+// Per-row sum-of-squares statistics are kept as ss_parts(d) partial sums, one per 256-column
+// n-tile of the producing GEMM (GEMM_BN), stored [part][row] with a row stride.
+__host__ __device__ inline int ss_parts(int d_model) { return (d_model + 255) / 256; }
 int gemm_smem_bytes();
 int gemm_cta_group();   // 2 (default) or 1 via PF_GEMM_CTAS=1
 bool make_weight_tmap(CUtensorMap* out, const void* B, int N, int K, int ldb);
@@ -63,6 +67,8 @@ int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, void* h
                  int d, cudaStream_t stream);
 int launch_rmsnorm(const float* resid, const float* gamma, void* out_bf16, int T, int d, float eps,
                    cudaStream_t stream);
+int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* lo, const float* ss, int ss_ld,
+                        const float* g, int d, float eps, float* out, cudaStream_t stream);
 int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const void* hi,
                        const void* lo, int d, void* attn_c, void* hi_c, void* lo_c, cudaStream_t stream);
 // resid (fp32) or, when resid == nullptr, the bf16 (hi, lo) pair

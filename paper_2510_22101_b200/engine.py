@@ -146,6 +146,39 @@ class PrefillScorer:
         _lib.check(rc)
         return logits2, p_yes
 
+    def score_capture(self, dp: DevicePacked, rows, gains, stream=None, return_scores=False, out=None):
+        """pf_score with the calibration capture (SPEC.md:200-203 capture flag): returns a device
+        fp32 tensor [n_layers, len(rows), d_model] of rmsnorm(x_l[row]) * gains[l], the MLP input
+        of every layer at the packed rows ``rows`` (device int32).  Synchronises ``stream``."""
+        import torch
+
+        cfg, pk = self.config, dp.packed
+        n = pk.n_items
+        rows = rows.to(device=self.device, dtype=torch.int32).contiguous()
+        if rows.numel() and (int(rows.min()) < 0 or int(rows.max()) >= pk.T):
+            raise ValueError("score_capture: capture rows outside [0, T)")
+        gains = gains.to(device=self.device, dtype=torch.float32).contiguous()
+        if tuple(gains.shape) != (cfg.n_layers, cfg.d_model):
+            raise ValueError("score_capture: gains must be [n_layers, d_model]")
+        shape = (cfg.n_layers, rows.numel(), cfg.d_model)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=self.device)
+        elif (tuple(out.shape) != shape or out.dtype != torch.float32 or out.device.type != "cuda"
+              or out.stride()[1:] != (cfg.d_model, 1)):
+            raise ValueError("score_capture: out must be fp32 [n_layers, n_rows, d_model], rows dense")
+        logits2 = torch.empty((n, 2), dtype=torch.float32, device=self.device)
+        p_yes = torch.empty((n,), dtype=torch.float32, device=self.device)
+        ws, ws_bytes = self.workspace(pk.T, n)
+        cap = _lib.PfCapture(rows=_ptr(rows), n_rows=rows.numel(), gains=_ptr(gains), out=_ptr(out),
+                             out_layer_stride=out.stride(0))
+        st = self._stream(stream)
+        rc = self.lib.pf_score_capture(self.handle, _ptr(dp.ids), _ptr(dp.pos), _ptr(dp.segs), len(pk.segs),
+                                       _ptr(dp.work), len(pk.work), _ptr(dp.last_idx), n, pk.T, ws, ws_bytes,
+                                       _ptr(logits2), _ptr(p_yes), _ptr(self._bad), ctypes.byref(cap), st)
+        _lib.check(rc)
+        (stream if stream is not None else torch.cuda.current_stream(self.device)).synchronize()
+        return (out, logits2, p_yes) if return_scores else out
+
     def graph_runner(self, dp: DevicePacked):
         """Capture one pf_score pass over ``dp`` into a CUDA graph (private workspace and output
         buffers, so later calls cannot invalidate it).  Returns ``run() -> (logits2, p_yes)``;

@@ -55,8 +55,18 @@ def _check_keep(keep: Sequence[int], n: int, what: str) -> np.ndarray:
     return k
 
 
-def prune_mlp_neurons(weights: Weights, keep: Sequence[Sequence[int]],
-                      w_down_rows: Sequence[np.ndarray] | None = None) -> Weights:
+def prune_mlp_neurons(weights: Weights, keep, w_down_rows=None) -> Weights:
+    """Two call forms:
+    * ``prune_mlp_neurons(weights, calib: CalibrationSet, sparsity)`` -- the reference signature
+      (SPEC.md:477): calibrated keep-sets + W_down refit (``calibration.py``, OSSCAR stand-in);
+    * ``prune_mlp_neurons(weights, keep_sets, w_down_rows=None)`` -- apply given per-layer keep-sets
+      (and optional refit rows): the shape contract the kernels consume."""
+    from .calibration import CalibrationSet, prune_mlp_neurons_calibrated
+
+    if isinstance(keep, CalibrationSet):
+        if w_down_rows is None:
+            raise ValueError("prune_mlp_neurons(weights, calib, sparsity): sparsity required")
+        return prune_mlp_neurons_calibrated(weights, keep, float(w_down_rows))
     cfg = weights.config
     if len(keep) != cfg.n_layers:
         raise ValueError("one keep-set per layer")

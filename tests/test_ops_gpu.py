@@ -161,13 +161,14 @@ def test_embed_rmsnorm_head(lib):
     resid = torch.empty(T, d, device="cuda")
     xb = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
     lo = torch.full((T, d), 7.0, device="cuda", dtype=torch.bfloat16)
-    ss = torch.empty(T, device="cuda")
+    ss = torch.full((d // 256, T), 5.0, device="cuda")       # partial-sum layout [part][T]
     _lib.check(lib.pf_embed(P(ids), P(emb), P(resid), P(xb), P(lo), P(ss), T, d, stream()))
     torch.cuda.synchronize()
     torch.testing.assert_close(resid, emb[ids.long()].float(), rtol=0, atol=0)
     torch.testing.assert_close(xb, emb[ids.long()], rtol=0, atol=0)
     assert float(lo.abs().max()) == 0.0
-    torch.testing.assert_close(ss, emb[ids.long()].float().pow(2).sum(-1), rtol=1e-5, atol=1e-3)
+    torch.testing.assert_close(ss[0], emb[ids.long()].float().pow(2).sum(-1), rtol=1e-5, atol=1e-3)
+    assert float(ss[1:].abs().max()) == 0.0
 
     x = torch.randn(T, d, device="cuda") * 3
     g = torch.rand(d, device="cuda") + 0.5
@@ -207,41 +208,45 @@ def gemm_ex(lib, **kw):
 @pytest.mark.parametrize("M,N,K", [(1000, 256, 128), (5000, 2048, 1280), (700, 384, 256)])
 def test_gemm_resid_add_norm(lib, M, N, K):
     """Fused RMSNorm producer on the bf16 residual pair x = hi + lo: x += A.B^T in place
-    (hi = bf16(x), lo = bf16(x - hi)), ss_out += row sum of squares of the new x."""
+    (hi = bf16(x), lo = bf16(x - hi)); ss_out[nb] = row sum of squares of the new x over n-tile nb
+    (256 columns; deterministic partials, no atomics)."""
     A = rand_bf16(M, K, seed=30)
     B = rand_bf16(N, K, scale=K ** -0.5, seed=31)
     x0 = torch.randn(M, N, device="cuda") * 4
     hi = x0.to(torch.bfloat16)
     lo = (x0 - hi.float()).to(torch.bfloat16)
     x0 = hi.float() + lo.float()
-    ss = torch.full((M,), 0.25, device="cuda")
+    parts = (N + 255) // 256
+    ss = torch.full((parts, M + 3), 0.25, device="cuda")     # row stride M + 3: ss_ld honoured
     gemm_ex(lib, A=A, lda=K, B=B, ldb=K, C=lo, ldc=N, M=M, N=N, K=K, epilogue=_lib.EPI_RESID_ADD_NORM,
-            xb=hi, ldxb=N, ss_out=ss)
+            xb=hi, ldxb=N, ss_out=ss, ss_ld=M + 3)
     ref = x0 + A.float() @ B.float().t()
     x = hi.float() + lo.float()
     torch.testing.assert_close(x, ref, rtol=2e-5, atol=2e-5)          # pair keeps ~16 mantissa bits
     assert bool(((hi.float() - x).abs() <= x.abs() * 2.0 ** -8 + 1e-30).all())   # hi = bf16(x), half-ulp
-    torch.testing.assert_close(ss, 0.25 + ref.pow(2).sum(-1), rtol=1e-4, atol=1e-2)
+    for p in range(parts):
+        torch.testing.assert_close(ss[p, :M], ref[:, 256 * p:256 * (p + 1)].pow(2).sum(-1), rtol=1e-4, atol=1e-2)
+    assert float((ss[:, M:] - 0.25).abs().max()) == 0.0
 
 
 def test_gemm_row_scaled_swiglu_and_rope(lib):
-    """Fused RMSNorm consumer: the accumulator row is scaled by rsqrt(ss/d + eps) before the
-    SwiGLU / RoPE epilogues; ss_zero rows are cleared."""
-    M, K, F = 900, 256, 384
+    """Fused RMSNorm consumer: the accumulator row is scaled by rsqrt(sum of the ceil(K/256)
+    partial sums of squares / d + eps) before the SwiGLU / RoPE epilogues."""
+    M, K, F = 900, 512, 384
     x = torch.randn(M, K, device="cuda") * 3
     xb = x.to(torch.bfloat16)
     ss_in = xb.float().pow(2).sum(-1)
-    zero_me = torch.ones(M, device="cuda")
+    frac = torch.rand(M, device="cuda")
+    ss_parts = torch.stack([ss_in * frac, ss_in * (1 - frac)]).contiguous()   # [2][M]
     G = rand_bf16(F, K, scale=K ** -0.5, seed=32)
     U = rand_bf16(F, K, scale=K ** -0.5, seed=33)
     B = interleave_gate_up(G, U, F).contiguous()
     C = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
     gemm_ex(lib, A=xb, lda=K, B=B, ldb=K, C=C, ldc=F, M=M, N=2 * F, K=K, epilogue=_lib.EPI_SWIGLU,
-            row_ss=ss_in, ss_zero=zero_me, inv_d=1.0 / K, eps=1e-6)
+            row_ss=ss_parts, inv_d=1.0 / K, eps=1e-6)
     xn = xb.float() * torch.rsqrt(ss_in / K + 1e-6)[:, None]
     ref = torch.nn.functional.silu(xn @ G.float().t()) * (xn @ U.float().t())
     torch.testing.assert_close(C.float(), ref, rtol=2e-2, atol=2e-2)
-    assert float(zero_me.abs().max()) == 0.0
 
     cfg = ModelConfig(n_layers=1, d_model=K, n_heads=2, n_kv_heads=1, d_ff=128, d_head=128)
     cos, sin = (torch.from_numpy(t).cuda() for t in rope_tables(cfg))
@@ -249,7 +254,7 @@ def test_gemm_row_scaled_swiglu_and_rope(lib):
     pos = torch.randint(0, 2048, (M,), device="cuda", dtype=torch.int32)
     Cq = torch.empty(M, 512, device="cuda", dtype=torch.bfloat16)
     gemm_ex(lib, A=xb, lda=K, B=Bq, ldb=K, C=Cq, ldc=512, M=M, N=512, K=K, epilogue=_lib.EPI_ROPE_BF16,
-            pos=pos, rope_cos=cos, rope_sin=sin, rope_heads=3, row_ss=ss_in, inv_d=1.0 / K, eps=1e-6)
+            pos=pos, rope_cos=cos, rope_sin=sin, rope_heads=3, row_ss=ss_parts, inv_d=1.0 / K, eps=1e-6)
     refq = rope_ref(xn @ Bq.float().t(), pos, cos, sin, 3)
     torch.testing.assert_close(Cq.float(), refq, rtol=1.6e-2, atol=2e-2)
 

@@ -281,3 +281,18 @@ def golden_ids(case, budget):
     from paper_2510_22101_b200 import ingest
 
     return ingest.encode(case["truncated"][budget])
+
+
+def test_forward_bit_reproducible_full_width():
+    """d_model 2048 = 8 n-tiles of row sum-of-squares partials: they are stored per tile and
+    summed in a fixed order (no atomics), so two passes give bit-identical scores."""
+    cfg = CONFIGS["C4"]
+    from paper_2510_22101_b200 import init_device_weights
+
+    scorer = PrefillScorer(init_device_weights(cfg, 0, "cuda"))
+    rng = np.random.default_rng(6)
+    packed = pack_requests([make_shared(rng, 64, [100] * 48, "spread")])
+    a = scorer.score_packed(packed)
+    b = scorer.score_packed(packed)
+    np.testing.assert_array_equal(a.logits2, b.logits2)
+    np.testing.assert_array_equal(a.p_yes, b.p_yes)

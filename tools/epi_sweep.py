@@ -19,7 +19,7 @@ st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 M, N, fused = a.m, a.n, EPIS[a.epi]
 xb = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
 out = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-ss = torch.ones(M, device="cuda")
+ss = torch.ones(32, M, device="cuda")   # partial sums [part][M], parts = ceil(N or K / 256)
 pos = torch.randint(0, 2048, (M,), device="cuda", dtype=torch.int32)
 cs = torch.rand(2048, 64, device="cuda")
 for K in [int(k) for k in a.ks.split(",")]:

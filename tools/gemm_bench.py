@@ -70,7 +70,7 @@ def main():
         C = torch.zeros(M, ncol, device="cuda", dtype=torch.float32 if epi == _lib.EPI_RESID_ADD else torch.bfloat16)
 
         xb = torch.empty(M, ncol, device="cuda", dtype=torch.bfloat16) if epi == _lib.EPI_RESID_ADD_NORM else None
-        ss = torch.ones(M, device="cuda")
+        ss = torch.ones(32, M, device="cuda")   # partial sums [part][M]
         args = _lib.PfGemmArgs(A=A.data_ptr(), lda=K, B=B.data_ptr(), ldb=K, C=C.data_ptr(), ldc=ncol, M=M, N=N,
                                K=K, epilogue=epi, pos=pos.data_ptr() if epi == 1 else None,
                                rope_cos=cos.data_ptr(), rope_sin=sin.data_ptr(), rope_heads=(N // 128) * 3 // 4 if epi == 1 else 0,

@@ -16,7 +16,7 @@ for n, M, N, K, epi, _ in gb.SHAPES:
     ncol = N // 2 if epi == _lib.EPI_SWIGLU else N
     C = torch.zeros(M, ncol, device="cuda", dtype=torch.float32 if epi == 3 else torch.bfloat16)
     xb = torch.empty(M, ncol, device="cuda", dtype=torch.bfloat16)
-    ss = torch.ones(M, device="cuda")
+    ss = torch.ones(32, M, device="cuda")   # partial sums [part][M]
     pos = torch.zeros(M, device="cuda", dtype=torch.int32)
     cs = torch.ones(2048, 64, device="cuda")
     a = _lib.PfGemmArgs(A=A.data_ptr(), lda=K, B=B.data_ptr(), ldb=K, C=C.data_ptr(), ldc=ncol, M=M, N=N, K=K,
