@@ -20,8 +20,10 @@
 //   warp 9      TMEM owner + tcgen05.mma issuer: S_j = Q_j K^T (SS, M128 N64 K128),
 //               O_j += P_j V (TS: P from TMEM, V MN-major from smem, M128 N128 K64)
 //   warps 10-11 fill a shared-memory table with this CTA's unit descriptors at kernel start
-// TMEM columns: S_0 [0,64) S_1 [64,128) O_0 [128,256) O_1 [256,384) P_0 [384,448) P_1 [448,512)
-// (P double-buffered: the issuer runs S(b+1) before PV(b) so softmax(b+1) overlaps PV(b)).
+// TMEM columns: S_{j,buf} at 64 (2 j + buf) [0,256), O_j at 256 + DH j.  S is double-buffered per
+// head and P_j(b) (bf16 pairs, 32 columns) overwrites the first half of its own S buffer, so the
+// issuer runs S(b+1) while softmax(b) is still working: the softmax never waits for an MMA
+// (ncu: the single-buffered version spent ~30% of softmax time in the s_full wait).
 #include <cuda_runtime.h>
 #include "ptx.cuh"
 #include "pf_internal.h"
@@ -48,9 +50,9 @@ struct AtCfg {
   static constexpr int OST_WARP = NBX * 32 * 128;
   static constexpr int OFF_TAB = OFF_OST + 8 * OST_WARP;
   static constexpr int OFF_BAR = OFF_TAB + AT_TAB * 48;
-  static constexpr int SMEM = 1024 + OFF_BAR + 160;
-  // TMEM columns: S_j at 64 j, O_j at 128 + DH j, P_j[buf] at 128 + 2 DH + 64 j + 32 buf
-  static constexpr uint32_t TS = 0, TO = 128, TP = 128 + 2 * DH;
+  static constexpr int SMEM = 1024 + OFF_BAR + 192;
+  // TMEM columns: S_{j,buf} (and P_j over it) at 64 (2 j + buf), O_j at 256 + DH j
+  static constexpr uint32_t TS = 0, TO = 256;
 };
 
 // ---- debug trace (pf_debug_set_trace): CTA 0 appends {event, unit, block, ns} records
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   constexpr int AT_Q_HEAD = C::Q_HEAD, AT_Q_BUF = C::Q_BUF, AT_KV_STAGE = C::KV_STAGE;
   constexpr int AT_OFF_KV = C::OFF_KV, AT_OFF_OST = C::OFF_OST, AT_OST_WARP = C::OST_WARP;
   constexpr int AT_OFF_TAB = C::OFF_TAB, AT_OFF_BAR = C::OFF_BAR;
-  constexpr uint32_t AT_TS = C::TS, AT_TO = C::TO, AT_TP = C::TP;
+  constexpr uint32_t AT_TS = C::TS, AT_TO = C::TO;
   constexpr int NBX = C::NBX;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -117,11 +119,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   uint64_t* q_empty = bars + 2;            // [2]
   uint64_t* kv_full = bars + 4;            // [3]
   uint64_t* kv_empty = bars + 7;           // [3]
-  uint64_t* s_full = bars + 10;            // [2]
-  uint64_t* p_ready = bars + 12;           // [2]
-  uint64_t* o_done = bars + 14;            // [2]
-  uint64_t* pv_done = bars + 16;           // [2]  one phase per PV_j
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* s_full = bars + 10;            // [4]  [head j][S buffer]
+  uint64_t* p_ready = bars + 14;           // [2]
+  uint64_t* o_done = bars + 16;            // [2]
+  uint64_t* pv_done = bars + 18;           // [2]  one phase per PV_j
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -134,7 +136,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tma_prefetch_desc(&tmO);
     for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
     for (int s = 0; s < AT_STAGES; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int j = 0; j < 2; ++j) { mbar_init(&s_full[j], 1); mbar_init(&p_ready[j], 4); mbar_init(&o_done[j], 1); mbar_init(&pv_done[j], 1); }
+    for (int j = 0; j < 4; ++j) mbar_init(&s_full[j], 1);
+    for (int j = 0; j < 2; ++j) { mbar_init(&p_ready[j], 4); mbar_init(&o_done[j], 1); mbar_init(&pv_done[j], 1); }
     fence_barrier_init();
   }
   if (warp >= 10) {   // unit-descriptor table: one global round trip per CTA instead of per unit
@@ -192,70 +195,77 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   } else if (warp == 9) {
     // ---------------------------------------------------------------------- MMA issuer
     // Warp-converged loop (uniform descriptors in uniform registers); one elected lane issues.
-    // Software-pipelined: once softmax_j has consumed S_j(b) (p_ready), S_j(b+1) is issued ahead
-    // of PV_j(b), so the tensor core computes the next scores while softmax_j waits for nothing.
+    // Per head j, S blocks are numbered globally (sc[j]) and alternate between two TMEM buffers;
+    // S(g) may overwrite buffer g&1 once PV(g-2), which read P from it, has completed.  The issuer
+    // waits for the latest PV it issued (never an older phase, so the parity wait cannot alias).
+    // Order per block b: PV_j(b) as soon as softmax_j(b) hands P over, then S_j(b+2).
     constexpr uint32_t idesc_s = make_idesc_bf16(128, AT_KB, false, false);
     constexpr uint32_t idesc_o = make_idesc_bf16(128, DH, false, true);    // V is MN-major
-    uint32_t kv_it = 0, q_it = 0, blk0 = 0, blk1 = 0;
+    uint32_t kv_it = 0, q_it = 0;
+    uint32_t sc[2] = {0u, 0u}, pc[2] = {0u, 0u};   // S blocks / PVs issued per head (global)
     const uint64_t q_desc = kmajor_desc(smem_u32(sQ));
     int k = 0;
-    auto issue_s = [&](int j, uint32_t st) {
-      const uint64_t k_desc = kmajor_desc(smem_u32(sKV + st * AT_KV_STAGE));
-#pragma unroll
-      for (int kk = 0; kk < DH / 16; ++kk) {   // descriptor start field is in 16-byte units
-        const uint32_t qo = (j * AT_Q_HEAD + (kk >> 2) * AT_QBOX + (kk & 3) * 32) >> 4;
-        const uint32_t ko = ((kk >> 2) * AT_KBOX + (kk & 3) * 32) >> 4;
-        umma_bf16_ss(tmem_base + AT_TS + j * AT_KB, q_desc + qo, k_desc + ko, idesc_s, kk != 0);
-      }
-      umma_commit(&s_full[j]);
-    };
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++k) {
       const UnitInfo ui = unit(u, k);
       mbar_wait(&q_full[0], q_it & 1);
       att_trace(EV_QFULL, k, 0, 9);
-      // prologue: S(0) for both heads
-      uint32_t st = kv_it % AT_STAGES;
-      mbar_wait(&kv_full[st], (kv_it / AT_STAGES) & 1);
-      att_trace(EV_KVFULL, k, 0, 9);
-      tc_fence_after();
-      if (elect_one()) {
-        for (int j = 0; j < ui.nh; ++j) issue_s(j, st);
-        if (ui.n_blk == 1) umma_commit(&q_empty[0]);
-      }
-      __syncwarp();
+      // S_j(b) for every head of the unit: K/V block b resident, target buffer free
+      auto issue_s_block = [&](int b) {
+        const uint32_t st = (kv_it + b) % AT_STAGES;
+        mbar_wait(&kv_full[st], ((kv_it + b) / AT_STAGES) & 1);
+        att_trace(EV_KVFULL, k, b, 9);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j < ui.nh && sc[j] >= 2) mbar_wait(&pv_done[j], (pc[j] - 1) & 1);   // PV(sc-2) (or later) done
+        }
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t k_desc = kmajor_desc(smem_u32(sKV + st * AT_KV_STAGE));
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (j >= ui.nh) break;
+            const uint32_t buf = sc[j] & 1;
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk) {   // descriptor start field is in 16-byte units
+              const uint32_t qo = (j * AT_Q_HEAD + (kk >> 2) * AT_QBOX + (kk & 3) * 32) >> 4;
+              const uint32_t ko = ((kk >> 2) * AT_KBOX + (kk & 3) * 32) >> 4;
+              umma_bf16_ss(tmem_base + AT_TS + 64 * (2 * j + buf), q_desc + qo, k_desc + ko, idesc_s, kk != 0);
+            }
+            umma_commit(&s_full[2 * j + buf]);
+          }
+          if (b == ui.n_blk - 1) umma_commit(&q_empty[0]);   // the unit's last S has read Q
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sc[j] += j < ui.nh ? 1u : 0u;
+      };
+      issue_s_block(0);
+      if (ui.n_blk > 1) issue_s_block(1);
       for (int b = 0; b < ui.n_blk; ++b) {
         const uint32_t st_b = (kv_it + b) % AT_STAGES;
-        const bool more = b + 1 < ui.n_blk;
-        const uint32_t st_n = (kv_it + b + 1) % AT_STAGES;
-        if (more) {
-          mbar_wait(&kv_full[st_n], ((kv_it + b + 1) / AT_STAGES) & 1);
-          att_trace(EV_KVFULL, k, b + 1, 9);
-        }
         const uint32_t v_addr = smem_u32(sKV + st_b * AT_KV_STAGE) + NBX * AT_KBOX;
-        for (int j = 0; j < ui.nh; ++j) {
-          uint32_t& bi = j == 0 ? blk0 : blk1;
-          const uint32_t pbuf = bi & 1;
-          mbar_wait(&p_ready[j], bi & 1);
-          ++bi;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j >= ui.nh) break;
+          mbar_wait(&p_ready[j], pc[j] & 1);
           att_trace(EV_PREADY, k, b, 9 + 16 * j);
           tc_fence_after();
+          const uint32_t tp = tmem_base + AT_TS + 64 * (2 * j + (pc[j] & 1));   // P_j(b) over S buffer
           if (elect_one()) {
-            if (more) {
-              issue_s(j, st_n);
-              if (b + 1 == ui.n_blk - 1 && j == ui.nh - 1) umma_commit(&q_empty[0]);
-            }
 #pragma unroll
             for (int kk = 0; kk < AT_KB / 16; ++kk) {
-              umma_bf16_ts(tmem_base + AT_TO + j * DH, tmem_base + AT_TP + j * 64 + pbuf * 32 + kk * 8,
-                           sw128_desc(v_addr + kk * 2048, AT_KBOX, 1024), idesc_o, (b | kk) != 0);
+              umma_bf16_ts(tmem_base + AT_TO + j * DH, tp + kk * 8, sw128_desc(v_addr + kk * 2048, AT_KBOX, 1024),
+                           idesc_o, (b | kk) != 0);
             }
             umma_commit(&pv_done[j]);
-            if (!more) umma_commit(&o_done[j]);
+            if (b == ui.n_blk - 1) umma_commit(&o_done[j]);
           }
           __syncwarp();
+          ++pc[j];
         }
-        if (elect_one()) umma_commit(&kv_empty[st_b]);
+        if (elect_one()) umma_commit(&kv_empty[st_b]);   // S(b) and PV(b) of every head have read it
         __syncwarp();
+        if (b + 2 < ui.n_blk) issue_s_block(b + 2);
       }
       kv_it += ui.n_blk;
       ++q_it;
@@ -265,9 +275,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int j = warp >> 2;
     const uint32_t row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem_base + lane_base + AT_TS + j * AT_KB;
+    const uint32_t tS0 = tmem_base + lane_base + AT_TS + 64 * (2 * j);   // + 64 * buf
     const uint32_t tO = tmem_base + lane_base + AT_TO + j * DH;
-    const uint32_t tP = tmem_base + lane_base + AT_TP + j * 64;
     const float sl2 = d.scale * 1.4426950408889634f;
     uint32_t blk_it = 0, u_it = 0;
     int k = 0;
@@ -280,7 +289,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const bool is_pre = b < ui.n_pre;
         const int lim = is_pre ? (ui.kv_len - b * AT_KB) : (q_local - (b - ui.n_pre) * AT_KB + 1);
         const bool full = __all_sync(0xffffffffu, lim >= AT_KB);
-        mbar_wait(&s_full[j], blk_it & 1);
+        const uint32_t tS = tS0 + 64 * (blk_it & 1);
+        mbar_wait(&s_full[2 * j + (blk_it & 1)], (blk_it >> 1) & 1);
         if (lane == 0 && (warp & 3) == 0) att_trace(EV_SFULL, k, b, j);
         tc_fence_after();
         uint32_t s[2][32];
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const bool rescale = __any_sync(0xffffffffu, need);
         const float m_old = m_used;
         if (rescale) m_used = fmaxf(m_used, mx);
-        // P = exp2(s*scale - m_used) -> bf16 pairs -> TMEM (double-buffered; PV(n-1) read the other buffer)
+        // P = exp2(s*scale - m_used) -> bf16 pairs -> TMEM (over S; PV(b-1) read the other buffer)
         float sumv[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t w[32];
         const float neg_m = -m_used;
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             sumv[i & 3] += p0 + p1;                // 4 independent chains
             w[c * 16 + i] = pack_bf16x2(p0, p1);   // TMEM A operand: 2 keys per 32-bit column
           }
-        tmem_st_32x32b_x32(tP + (blk_it & 1) * 32, w);
+        tmem_st_32x32b_x32(tS, w);   // P_j(b) over the first half of its own S buffer
         // Every PV phase is consumed in order: PV of this head's previous block (issued right
         // after this block's S) has finished by now, so this wait is ~free; it also guards O.
         // (A unit's last PV phase is consumed in its epilogue.)

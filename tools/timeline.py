@@ -23,7 +23,7 @@ EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add", "4
 
 
 def key(name):
-    m = re.search(r"gemm_bf16_kernel<(\d)", name)
+    m = re.search(r"gemm_bf16_kernel<(?:\(int\))?(\d)", name)
     if m:
         return f"gemm<{EPI[m.group(1)]}>"
     return re.sub(r"^void |pf::|\(.*", "", name).split("<")[0]
