@@ -221,9 +221,9 @@ def run_ours(args):
     # executed work: the last layer's O-projection + MLP run on the n_items last-token rows only
     flops_exec = flops_step - shape.n_requests * (packed.T // shape.n_requests - shape.n_items) * 2 * (
         cfg.q_width * cfg.d_model + 3 * cfg.d_model * cfg.d_ff)
-    # embed + (L-1) x [QKV, attention, O, gate/up, down] + last layer [QKV, attention, gather, O,
-    # gate/up, down] + head  (RMSNorm is fused into the GEMM epilogues)
-    launches_per_step = 5 * cfg.n_layers + 3
+    # embed + rope-gather + (L-1) x [QKV, attention, O, gate/up, down] + last layer [QKV, attention,
+    # gather, O, gate/up, down] + head  (RMSNorm is fused into the GEMM epilogues)
+    launches_per_step = 5 * cfg.n_layers + 4
 
     def barrier():
         if ws > 1:

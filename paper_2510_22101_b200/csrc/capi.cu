@@ -101,6 +101,7 @@ struct Workspace {
   void* rlo;         // lo
   float* ss_attn;    // per-row partial sums of squares of the residual feeding the attention block
   float* ss_mlp;     // ... feeding the MLP block ([ss_parts(d)][T], see pf_internal.h)
+  float* rope_cs;    // per-row cos/sin gathered for the QKV epilogue (launch_rope_gather layout)
   void* qkv;
   void* attn;
   void* hbuf;
@@ -123,6 +124,7 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   w.rlo = take((size_t)T * d.d_model * 2);
   w.ss_attn = reinterpret_cast<float*>(take((size_t)ss_parts(d.d_model) * T * 4));   // [part][T]
   w.ss_mlp = reinterpret_cast<float*>(take((size_t)ss_parts(d.d_model) * T * 4));
+  w.rope_cs = reinterpret_cast<float*>(take(rope_gather_floats(T, d.d_head / 2) * 4));
   w.qkv = take((size_t)T * m->qkv_n * 2);
   w.attn = take((size_t)T * m->attn_k * 2);
   w.hbuf = take((size_t)T * d.d_ff_pad * 2);
@@ -221,12 +223,15 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
   // w_qkv / w_gu by the caller, include/prefill_sm100.h).
   int rc = launch_embed(ids, d.embedding, nullptr, w.xb, w.rlo, w.ss_attn, T, d.d_model, st);
   if (rc) return rc;
+  // positions are fixed for the pass: gather each row's cos/sin once into the coalesced layout
+  if ((rc = launch_rope_gather(pos, d.rope_cos, d.rope_sin, d.d_head / 2, T, w.rope_cs, st))) return rc;
   for (int l = 0; l < d.n_layers; ++l) {
     GemmDesc g{};
     g.A = w.xb; g.lda = d.d_model; g.B = d.w_qkv[l]; g.ldb = d.d_model;
     g.C = w.qkv; g.ldc = m->qkv_n; g.M = T; g.N = m->qkv_n; g.K = d.d_model;
     g.epilogue = EPI_ROPE_BF16; g.pos = pos; g.rope_cos = d.rope_cos; g.rope_sin = d.rope_sin;
     g.rope_heads = d.n_heads + d.n_kv_heads; g.rope_dh = d.d_head; g.max_seq = d.max_seq;
+    g.rope_cs = w.rope_cs;
     g.row_ss = w.ss_attn; g.ss_ld = T; g.inv_d = inv_d; g.eps = eps;
     if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
     AttnDesc a{};

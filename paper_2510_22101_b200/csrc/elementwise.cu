@@ -201,6 +201,36 @@ __global__ void __launch_bounds__(256) capture_rows_kernel(const int32_t* __rest
   }
 }
 
+// RoPE cos/sin gathered per packed row (layout in pf_internal.h): warp = (32-row group, quad),
+// lane = row, so every store is 512 contiguous bytes; rows past T use position 0.
+__global__ void __launch_bounds__(256) rope_gather_kernel(const int32_t* __restrict__ pos,
+                                                          const float4* __restrict__ cos_tab,
+                                                          const float4* __restrict__ sin_tab, int qn, int T,
+                                                          int n_groups, float4* __restrict__ out) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5);   // (group, quad) pair
+  const int lane = threadIdx.x & 31;
+  if (w >= n_groups * qn) return;
+  const int g = w / qn, q = w - (w / qn) * qn;
+  const int row = g * 32 + lane;
+  const size_t p = row < T ? (size_t)__ldg(pos + row) : 0;
+  out[((size_t)(g * 2 + 0) * qn + q) * 32 + lane] = __ldg(cos_tab + p * qn + q);
+  out[((size_t)(g * 2 + 1) * qn + q) * 32 + lane] = __ldg(sin_tab + p * qn + q);
+}
+
+int launch_rope_gather(const int32_t* pos, const float* cos_tab, const float* sin_tab, int half, int T,
+                       float* out, cudaStream_t stream) {
+  if (T == 0) return 0;
+  if (half % 4 != 0) return fail(-2, "rope_gather: d_head/2 must be a multiple of 4");
+  const int qn = half / 4, n_groups = (T + 31) / 32;
+  rope_gather_kernel<<<(n_groups * qn + 7) / 8, 256, 0, stream>>>(
+      pos, reinterpret_cast<const float4*>(cos_tab), reinterpret_cast<const float4*>(sin_tab), qn, T, n_groups,
+      reinterpret_cast<float4*>(out));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "rope_gather launch: %s", cudaGetErrorString(e));
+}
+
 int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* lo, const float* ss, int ss_ld,
                         const float* g, int d, float eps, float* out, cudaStream_t stream) {
   if (n == 0) return 0;

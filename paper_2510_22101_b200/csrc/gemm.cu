@@ -62,8 +62,9 @@ struct GemmArgs {
   int M, N, K;
   int num_m_blk, num_n_blk;
   const int32_t* pos;      // EPI_ROPE: position per row
-  const float* rope_cos;   // [max_seq x 64]
+  const float* rope_cos;   // [max_seq x dh/2]
   const float* rope_sin;
+  const float* rope_cs;    // gathered per-row cos/sin (launch_rope_gather layout) or null
   int rope_heads;          // heads (of rope_dh cols) that receive RoPE
   int rope_dh;             // head width: 64 or 128
   const float* row_ss;     // fused RMSNorm: per-row partial sums of squares [ss_parts_in][ss_ld] (or null)
@@ -426,8 +427,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int cpb = half / 32;                    // 32-col blocks per head half (1 or 2)
         const int n_items = GEMM_BN / 32 / 2;         // 4 for both head widths
         const int p = rvalid ? __ldg(args.pos + grow) : 0;
-        const float4* cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * half);
-        const float4* sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
+        // cos/sin of this row: gathered layout (coalesced: quad q of the warp's 32 rows is 512
+        // contiguous bytes, stride 32 float4) or the tables' row p (32 lines per warp load)
+        const int qn = half / 4;
+        const bool gathered = args.rope_cs != nullptr;
+        const float4* cs4;
+        const float4* sn4;
+        int qstride;
+        if (gathered) {
+          cs4 = reinterpret_cast<const float4*>(args.rope_cs) + (size_t)(r0 / 32) * 2 * qn * 32 + lane;
+          sn4 = cs4 + (size_t)qn * 32;
+          qstride = 32;
+        } else {
+          cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * half);
+          sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
+          qstride = 1;
+        }
         const uint32_t stg0 = smem_u32(my_stg);
         uint32_t x1[32], x2[32];
         tmem_ld_32x32b_x32(t_row, x1);
@@ -435,12 +450,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
         for (int it = 0; it < n_items; ++it) {
           const int hd = it / cpb, c = it % cpb;
-          const bool rot = ((n0 + hd * dh) / dh) < args.rope_heads;
+          // rows past M are padding: skip the rotation (the gathered table ends at ceil(M/32) groups)
+          const bool rot = ((n0 + hd * dh) / dh) < args.rope_heads && r0 < args.M;
           float4 cv[8], sv[8];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            cv[j4] = rot ? __ldg(cs4 + c * 8 + j4) : make_float4(1.f, 1.f, 1.f, 1.f);
-            sv[j4] = rot ? __ldg(sn4 + c * 8 + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            cv[j4] = rot ? __ldg(cs4 + (c * 8 + j4) * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
+            sv[j4] = rot ? __ldg(sn4 + (c * 8 + j4) * qstride) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
           tmem_ld_wait();
           uint32_t w1[16], w2[16];
@@ -618,6 +634,7 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
   a.M = d.M; a.N = d.N; a.K = d.K;
   a.num_n_blk = (d.N + GEMM_BN - 1) / GEMM_BN;
   a.pos = d.pos; a.rope_cos = d.rope_cos; a.rope_sin = d.rope_sin; a.rope_heads = d.rope_heads;
+  a.rope_cs = d.rope_cs;
   a.rope_dh = d.rope_dh == 64 ? 64 : 128;
   a.row_ss = d.row_ss; a.ss_out = d.ss_out;
   a.ss_parts_in = ss_parts(d.K);

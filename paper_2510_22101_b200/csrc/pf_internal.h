@@ -41,6 +41,9 @@ struct GemmDesc {
   const int32_t* pos;
   const float* rope_cos;
   const float* rope_sin;
+  // optional: cos/sin pre-gathered per packed row in the coalesced layout of launch_rope_gather
+  // (the forward builds it once per pass); null -> the epilogue reads the tables per row
+  const float* rope_cs;
   int rope_heads;
   int rope_dh;     // head width for the RoPE epilogue (64 or 128; 0 -> 128)
   int max_seq;
@@ -67,6 +70,12 @@ int launch_embed(const int32_t* ids, const void* emb_bf16, float* resid, void* h
                  int d, cudaStream_t stream);
 int launch_rmsnorm(const float* resid, const float* gamma, void* out_bf16, int T, int d, float eps,
                    cudaStream_t stream);
+// Per-row RoPE cos/sin gathered for the QKV epilogue: for row group g (32 rows), table t (0 cos,
+// 1 sin), quad q (4 frequencies), lane l:  out[(((g*2 + t)*(half/4) + q)*32 + l)*4 + e] =
+// tab_t[pos[32 g + l]][4 q + e].  A warp's float4 load of one quad is then 512 contiguous bytes.
+int launch_rope_gather(const int32_t* pos, const float* cos_tab, const float* sin_tab, int half, int T,
+                       float* out, cudaStream_t stream);
+inline size_t rope_gather_floats(int T, int half) { return (size_t)((T + 31) / 32) * 32 * 2 * half; }
 int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* lo, const float* ss, int ss_ld,
                         const float* g, int d, float eps, float* out, cudaStream_t stream);
 int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const void* hi,
