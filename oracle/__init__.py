@@ -11,6 +11,10 @@ What it restates (all citations into /root/reference):
   prefixcache.py SPEC.md:240-309  split_shared_prefix / merge_attention / score_shared_batch /
                                   throughput_gain, plus the flat packer layout the device uses
   scoring.py     SPEC.md:311-343  relevance_score (Eq 2) / rank_items
+  calibration.py SPEC.md:458-485  capture_calibration sampling, direct least-squares greedy backward
+                                  elimination and the exhaustive optimum (OSSCAR stand-in checks)
+  tokenizer.py   pkg/src/prefrank/tokenizer.py  encode / encode_with_spans / word_id, restated as an
+                                  explicit scanner; pinned to the reference-generated goldens
   The reference package ships NO code for these modules: the model path is
   "parity unpinned" by reference-executed outputs.  It is pinned by the spec's known-answer
   examples and invariants (tests/test_oracle.py) and the token-id / prompt-structure golden
