@@ -296,3 +296,33 @@ def test_forward_bit_reproducible_full_width():
     b = scorer.score_packed(packed)
     np.testing.assert_array_equal(a.logits2, b.logits2)
     np.testing.assert_array_equal(a.p_yes, b.p_yes)
+
+
+def test_long_items_up_to_max_seq():
+    """Prompts of exactly max_seq = 2048 tokens (32 key blocks: a 64-token prefix + 1984-token
+    items), a long prefix with long items, and 1024-token items, in one packed launch."""
+    cfg, scorer, ow = get_models("TINY_GQA")
+    rng = np.random.default_rng(31)
+    batches = [make_shared(rng, 64, [1984, 1984, 7], "spread"),
+               make_shared(rng, 1500, [548, 300, 1], "spread"),
+               make_shared(rng, 10, [1024, 1000], "template")]
+    assert max(len(sb.prefix_tokens) + len(s) for sb in batches for s in sb.suffixes) == cfg.max_seq
+    res = score_shared_batch(scorer, batches)
+    p_ref = oracle_scores(ow, batches)
+    dp = np.abs(res.p_yes - p_ref)
+    print(f"max_seq items: max|dp|={dp.max():.2e}")
+    assert dp.max() <= TOL_P
+
+
+def test_c3_width_long_items():
+    """C3 widths (d 2048, 16/8 heads of 128, d_ff 6144) at 2 layers, 1024-token items: the
+    full-width GEMM tiles and the 17-block attention path against the oracle."""
+    cfg = CONFIGS["C3"].with_(n_layers=2)
+    scorer, ow = PrefillScorer(init_weights(cfg, 0)), OM.init_weights(cfg, 0)
+    rng = np.random.default_rng(12)
+    batches = [make_shared(rng, 64, [1024, 1024, 640], "spread")]
+    res = score_shared_batch(scorer, batches)
+    p_ref = oracle_scores(ow, batches)
+    dp = np.abs(res.p_yes - p_ref)
+    print(f"C3-width long items: max|dp|={dp.max():.2e}")
+    assert dp.max() <= TOL_P
