@@ -289,6 +289,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const bool is_pre = b < ui.n_pre;
         const int lim = is_pre ? (ui.kv_len - b * AT_KB) : (q_local - (b - ui.n_pre) * AT_KB + 1);
         const bool full = __all_sync(0xffffffffu, lim >= AT_KB);
+        // 32-key halves masked for every row of this warp (causal diagonal): P = 0 there without
+        // spending SFU work on exp(-inf)
+        const int lim_max = __reduce_max_sync(0xffffffffu, lim);
         const uint32_t tS = tS0 + 64 * (blk_it & 1);
         mbar_wait(&s_full[2 * j + (blk_it & 1)], (blk_it >> 1) & 1);
         if (lane == 0 && (warp & 3) == 0) att_trace(EV_SFULL, k, b, j);
@@ -304,30 +307,45 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             for (int i = 0; i < 32; ++i)
               if (c * 32 + i >= lim) s[c][i] = __float_as_uint(-INFINITY);
         }
-        float mxv[8];
+        // row max with 3-input FMNMX (4 independent chains)
+        float mxv[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) mxv[i] = __uint_as_float(s[0][i]);
+        for (int i = 0; i < 4; ++i) mxv[i] = fmaxf(__uint_as_float(s[0][2 * i]), __uint_as_float(s[0][2 * i + 1]));
 #pragma unroll
-        for (int i = 8; i < 64; ++i) mxv[i & 7] = fmaxf(mxv[i & 7], __uint_as_float(s[i >> 5][i & 31]));
-        const float mx = sl2 * fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
-                                     fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
+        for (int i = 4; i < 32; ++i)
+          mxv[i & 3] = fmax3(mxv[i & 3], __uint_as_float(s[i >> 4][(2 * i) & 31]), __uint_as_float(s[i >> 4][(2 * i + 1) & 31]));
+        const float mx = sl2 * fmax3(fmaxf(mxv[0], mxv[1]), mxv[2], mxv[3]);
         const bool need = mx > m_used + AT_RESCALE_THRESH;
         const bool rescale = __any_sync(0xffffffffu, need);
         const float m_old = m_used;
         if (rescale) m_used = fmaxf(m_used, mx);
-        // P = exp2(s*scale - m_used) -> bf16 pairs -> TMEM (over S; PV(b-1) read the other buffer)
-        float sumv[4] = {0.f, 0.f, 0.f, 0.f};
+        // P = exp2(s*scale - m_used) -> bf16 pairs -> TMEM (over S; PV(b-1) read the other buffer).
+        // Key pairs go through FFMA2 / FADD2: ~3 issue slots per element instead of ~7.5.
+        uint64_t sum2[2] = {0ull, 0ull};
         uint32_t w[32];
-        const float neg_m = -m_used;
+        const uint64_t scale2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_used, -m_used);
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c) {
+          if (lim_max <= 32 * c) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[c * 16 + i] = 0u;
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float p0 = exp2f(fmaf(__uint_as_float(s[c][2 * i]), sl2, neg_m));
-            const float p1 = exp2f(fmaf(__uint_as_float(s[c][2 * i + 1]), sl2, neg_m));
-            sumv[i & 3] += p0 + p1;                // 4 independent chains
+            const uint64_t x2 =
+                ffma2(f2_pack(__uint_as_float(s[c][2 * i]), __uint_as_float(s[c][2 * i + 1])), scale2, negm2);
+            float x0, x1;
+            f2_unpack(x2, x0, x1);
+            const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+            sum2[i & 1] = fadd2(sum2[i & 1], f2_pack(p0, p1));
             w[c * 16 + i] = pack_bf16x2(p0, p1);   // TMEM A operand: 2 keys per 32-bit column
           }
+        }
+        float sa, sb, sc2, sd;
+        f2_unpack(sum2[0], sa, sb);
+        f2_unpack(sum2[1], sc2, sd);
+        const float bsum = (sa + sb) + (sc2 + sd);
         tmem_st_32x32b_x32(tS, w);   // P_j(b) over the first half of its own S buffer
         // Every PV phase is consumed in order: PV of this head's previous block (issued right
         // after this block's S) has finished by now, so this wait is ~free; it also guards O.
@@ -347,7 +365,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             tmem_st_32x32b_x32(tO + c * 32, o);
           }
         }
-        l_run += (sumv[0] + sumv[1]) + (sumv[2] + sumv[3]);
+        l_run += bsum;
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -373,24 +391,30 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(d.out) +
                                             (size_t)(ui.q_row0 + row) * (d.H * d.dh) + (ui.h0 + j) * d.dh);
 #pragma unroll 1
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld_32x32b_x32(tO + c * 32, o);
+      for (int c2 = 0; c2 < DH / 64; ++c2) {
+        uint32_t o2[2][32];   // two 32-column loads in flight per wait
+        tmem_ld_32x32b_x32(tO + c2 * 64, o2[0]);
+        tmem_ld_32x32b_x32(tO + c2 * 64 + 32, o2[1]);
         tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-          v.y = pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-          v.z = pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-          v.w = pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
-          if (warp_full) {
-            // 64-column SW128 box (c >> 1); 16 B chunk (c & 1) * 4 + q of this row
-            const uint32_t chunk = (c & 1) * 4 + q;
-            st_shared_v4(smem_u32(ost + (c >> 1) * 4096) + lane * 128 + ((chunk ^ (lane & 7)) << 4), v.x, v.y,
-                         v.z, v.w);
-          } else if (valid) {
-            dst[c * 4 + q] = v;
+        for (int h = 0; h < 2; ++h) {
+          const int c = 2 * c2 + h;
+          const uint32_t (&o)[32] = o2[h];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            v.y = pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            v.z = pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            v.w = pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            if (warp_full) {
+              // 64-column SW128 box (c >> 1); 16 B chunk (c & 1) * 4 + q of this row
+              const uint32_t chunk = (c & 1) * 4 + q;
+              st_shared_v4(smem_u32(ost + (c >> 1) * 4096) + lane * 128 + ((chunk ^ (lane & 7)) << 4), v.x, v.y,
+                           v.z, v.w);
+            } else if (valid) {
+              dst[c * 4 + q] = v;
+            }
           }
         }
       }

@@ -8,7 +8,7 @@ from paper_2510_22101_b200 import CONFIGS, REQUESTS, _lib, init_weights
 from paper_2510_22101_b200.engine import DevicePacked, PrefillScorer
 
 NAMES = {1: "QFULL", 2: "KVFULL", 3: "S_ISSUED", 4: "PREADY", 5: "PV_ISSUED", 6: "SFULL", 7: "PARRIVE",
-         8: "ODONE", 9: "EPI_DONE", 10: "UNIT_START"}
+         8: "ODONE", 9: "EPI_DONE", 10: "UNIT_START", 12: "EPI_WAITED", 13: "EPI_STAGED"}
 cfg = CONFIGS["C4"].with_(n_layers=1)
 shape = REQUESTS["C4"]
 scorer = PrefillScorer(init_weights(cfg, 0))
