@@ -55,20 +55,21 @@ struct AtCfg {
   static constexpr uint32_t TS = 0, TO = 256;
 };
 
-// ---- debug trace (pf_debug_set_trace): CTA 0 appends {event, unit, block, ns} records
-__device__ unsigned long long* g_att_trace = nullptr;
-__device__ unsigned int g_att_trace_n = 0;
-__device__ unsigned int g_att_trace_cap = 0;
+// ---- debug trace (pf_debug_set_trace): CTA 0 appends {event, unit, block, ns} records.  The
+// buffer pointer travels in the kernel parameters (a global-memory flag cost ~5% of the warp-stall
+// samples in the disabled state: one long-scoreboard load per call site).
+static unsigned long long* g_trace_buf = nullptr;
+static unsigned int g_trace_cap = 0;
 enum AttEvt { EV_QFULL = 1, EV_KVFULL, EV_S_ISSUED, EV_PREADY, EV_PV_ISSUED, EV_SFULL, EV_PARRIVE, EV_ODONE, EV_EPI_DONE,
               EV_UNIT_START, EV_END };
-PF_DEVICE void att_trace(int ev, int unit, int blk, int who) {
+PF_DEVICE void att_trace(const AttnDesc& d, int ev, int unit, int blk, int who) {
   // atomic-free: fixed slot per (role, unit, block, event) so tracing adds no round trips
-  if (g_att_trace == nullptr || blockIdx.x != 0 || (threadIdx.x & 31) != 0) return;
+  if (d.trace == nullptr || blockIdx.x != 0 || (threadIdx.x & 31) != 0) return;
   const int role = who == 8 ? 0 : (who == 9 || who == 25) ? 1 : 2 + (who & 1);
   if (unit >= 64 || blk >= 8) return;
   const unsigned int i = ((role * 64 + unit) * 8 + blk) * 16 + ev + (who == 25 ? 11 : 0);
-  if (i >= g_att_trace_cap) return;
-  g_att_trace[i] = ((unsigned long long)ev << 56) | ((unsigned long long)(who & 0xff) << 48) |
+  if (i >= d.trace_cap) return;
+  d.trace[i] = ((unsigned long long)ev << 56) | ((unsigned long long)(who & 0xff) << 48) |
                    ((unsigned long long)(unit & 0xff) << 40) | ((unsigned long long)(blk & 0xff) << 32) |
                    (globaltimer_ns() & 0xffffffffull);
 }
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++k) {
       const UnitInfo ui = unit(u, k);
       const int qb = 0;
-      att_trace(EV_UNIT_START, k, ui.n_blk, 8);
+      att_trace(d, EV_UNIT_START, k, ui.n_blk, 8);
       mbar_wait(&q_empty[qb], (q_it & 1) ^ 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(&q_full[qb], ui.nh * AT_Q_HEAD);
@@ -196,9 +197,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     // ---------------------------------------------------------------------- MMA issuer
     // Warp-converged loop (uniform descriptors in uniform registers); one elected lane issues.
     // Per head j, S blocks are numbered globally (sc[j]) and alternate between two TMEM buffers;
-    // S(g) may overwrite buffer g&1 once PV(g-2), which read P from it, has completed.  The issuer
-    // waits for the latest PV it issued (never an older phase, so the parity wait cannot alias).
-    // Order per block b: PV_j(b) as soon as softmax_j(b) hands P over, then S_j(b+2).
+    // S_j(g) overwrites buffer g&1, whose P_j(g-2) the PV issued just before it reads.  tcgen05.mma
+    // ops of one thread execute in issue order, so S_j(b+2) follows PV_j(b) with no completion wait
+    // (as CUTLASS's sm100 FMHA does).  Both heads' S(b+2) go out together after both PV(b): issuing
+    // per head as soon as its own PV is out was 6% slower at C3 (the heads drift and the 3-stage
+    // K/V ring is released by the slower one).
     constexpr uint32_t idesc_s = make_idesc_bf16(128, AT_KB, false, false);
     constexpr uint32_t idesc_o = make_idesc_bf16(128, DH, false, true);    // V is MN-major
     uint32_t kv_it = 0, q_it = 0;
@@ -208,39 +211,36 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++k) {
       const UnitInfo ui = unit(u, k);
       mbar_wait(&q_full[0], q_it & 1);
-      att_trace(EV_QFULL, k, 0, 9);
-      // S_j(b) for every head of the unit: K/V block b resident, target buffer free
-      auto issue_s_block = [&](int b) {
+      att_trace(d, EV_QFULL, k, 0, 9);
+      auto wait_kv = [&](int b) {   // K/V block b resident in its ring stage
         const uint32_t st = (kv_it + b) % AT_STAGES;
         mbar_wait(&kv_full[st], ((kv_it + b) / AT_STAGES) & 1);
-        att_trace(EV_KVFULL, k, b, 9);
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (j < ui.nh && sc[j] >= 2) mbar_wait(&pv_done[j], (pc[j] - 1) & 1);   // PV(sc-2) (or later) done
-        }
+        att_trace(d, EV_KVFULL, k, b, 9);
         tc_fence_after();
+      };
+      auto issue_s = [&](int b, int j) {   // S_j(b) = Q_j K(b)^T into S buffer sc[j] & 1
+        const uint32_t st = (kv_it + b) % AT_STAGES;
         if (elect_one()) {
           const uint64_t k_desc = kmajor_desc(smem_u32(sKV + st * AT_KV_STAGE));
+          const uint32_t buf = sc[j] & 1;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (j >= ui.nh) break;
-            const uint32_t buf = sc[j] & 1;
-#pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk) {   // descriptor start field is in 16-byte units
-              const uint32_t qo = (j * AT_Q_HEAD + (kk >> 2) * AT_QBOX + (kk & 3) * 32) >> 4;
-              const uint32_t ko = ((kk >> 2) * AT_KBOX + (kk & 3) * 32) >> 4;
-              umma_bf16_ss(tmem_base + AT_TS + 64 * (2 * j + buf), q_desc + qo, k_desc + ko, idesc_s, kk != 0);
-            }
-            umma_commit(&s_full[2 * j + buf]);
+          for (int kk = 0; kk < DH / 16; ++kk) {   // descriptor start field is in 16-byte units
+            const uint32_t qo = (j * AT_Q_HEAD + (kk >> 2) * AT_QBOX + (kk & 3) * 32) >> 4;
+            const uint32_t ko = ((kk >> 2) * AT_KBOX + (kk & 3) * 32) >> 4;
+            umma_bf16_ss(tmem_base + AT_TS + 64 * (2 * j + buf), q_desc + qo, k_desc + ko, idesc_s, kk != 0);
           }
-          if (b == ui.n_blk - 1) umma_commit(&q_empty[0]);   // the unit's last S has read Q
+          umma_commit(&s_full[2 * j + buf]);
+          if (b == ui.n_blk - 1 && j == ui.nh - 1) umma_commit(&q_empty[0]);   // the unit's last S has read Q
         }
         __syncwarp();
-#pragma unroll
-        for (int j = 0; j < 2; ++j) sc[j] += j < ui.nh ? 1u : 0u;
+        ++sc[j];
       };
-      issue_s_block(0);
-      if (ui.n_blk > 1) issue_s_block(1);
+      for (int b = 0; b < min(2, ui.n_blk); ++b) {
+        wait_kv(b);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (j < ui.nh) issue_s(b, j);
+      }
       for (int b = 0; b < ui.n_blk; ++b) {
         const uint32_t st_b = (kv_it + b) % AT_STAGES;
         const uint32_t v_addr = smem_u32(sKV + st_b * AT_KV_STAGE) + NBX * AT_KBOX;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         for (int j = 0; j < 2; ++j) {
           if (j >= ui.nh) break;
           mbar_wait(&p_ready[j], pc[j] & 1);
-          att_trace(EV_PREADY, k, b, 9 + 16 * j);
+          att_trace(d, EV_PREADY, k, b, 9 + 16 * j);
           tc_fence_after();
           const uint32_t tp = tmem_base + AT_TS + 64 * (2 * j + (pc[j] & 1));   // P_j(b) over S buffer
           if (elect_one()) {
@@ -259,13 +259,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             }
             umma_commit(&pv_done[j]);
             if (b == ui.n_blk - 1) umma_commit(&o_done[j]);
+            if (j == ui.nh - 1) umma_commit(&kv_empty[st_b]);   // S(b) and PV(b) of every head have read it
           }
           __syncwarp();
           ++pc[j];
         }
-        if (elect_one()) umma_commit(&kv_empty[st_b]);   // S(b) and PV(b) of every head have read it
-        __syncwarp();
-        if (b + 2 < ui.n_blk) issue_s_block(b + 2);
+        if (b + 2 < ui.n_blk) {
+          wait_kv(b + 2);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (j < ui.nh) issue_s(b + 2, j);
+        }
       }
       kv_it += ui.n_blk;
       ++q_it;
@@ -294,27 +298,37 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const int lim_max = __reduce_max_sync(0xffffffffu, lim);
         const uint32_t tS = tS0 + 64 * (blk_it & 1);
         mbar_wait(&s_full[2 * j + (blk_it & 1)], (blk_it >> 1) & 1);
-        if (lane == 0 && (warp & 3) == 0) att_trace(EV_SFULL, k, b, j);
+        if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_SFULL, k, b, j);
         tc_fence_after();
         uint32_t s[2][32];
         tmem_ld_32x32b_x32(tS, s[0]);
         tmem_ld_32x32b_x32(tS + 32, s[1]);
         tmem_ld_wait();
         if (!full) {
+          // only a half that is partly visible to this warp needs per-key masking: on the causal
+          // diagonal that is one 32x32 sub-block per warp (fully masked halves are skipped below)
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+          for (int c = 0; c < 2; ++c) {
+            if (lim_max <= 32 * c || __all_sync(0xffffffffu, lim >= 32 * c + 32)) continue;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (c * 32 + i >= lim) s[c][i] = __float_as_uint(-INFINITY);
+          }
         }
-        // row max with 3-input FMNMX (4 independent chains)
+        // row max with 3-input FMNMX (4 independent chains) over the halves this warp can see
+        // (an unmasked, fully hidden half holds keys of later rows or of another segment)
         float mxv[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) mxv[i] = fmaxf(__uint_as_float(s[0][2 * i]), __uint_as_float(s[0][2 * i + 1]));
 #pragma unroll
-        for (int i = 4; i < 32; ++i)
-          mxv[i & 3] = fmax3(mxv[i & 3], __uint_as_float(s[i >> 4][(2 * i) & 31]), __uint_as_float(s[i >> 4][(2 * i + 1) & 31]));
-        const float mx = sl2 * fmax3(fmaxf(mxv[0], mxv[1]), mxv[2], mxv[3]);
+        for (int i = 4; i < 16; ++i)
+          mxv[i & 3] = fmax3(mxv[i & 3], __uint_as_float(s[0][2 * i]), __uint_as_float(s[0][2 * i + 1]));
+        if (lim_max > 32) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            mxv[i & 3] = fmax3(mxv[i & 3], __uint_as_float(s[1][2 * i]), __uint_as_float(s[1][2 * i + 1]));
+        }
+        const float mx = lim_max > 0 ? sl2 * fmax3(fmaxf(mxv[0], mxv[1]), mxv[2], mxv[3]) : -INFINITY;
         const bool need = mx > m_used + AT_RESCALE_THRESH;
         const bool rescale = __any_sync(0xffffffffu, need);
         const float m_old = m_used;
@@ -370,12 +384,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_ready[j]);
-        if (lane == 0 && (warp & 3) == 0) att_trace(EV_PARRIVE, k, b, j);
+        if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_PARRIVE, k, b, j);
       }
       // ---- unit epilogue: O / l -> bf16 -> global
       mbar_wait(&o_done[j], u_it & 1);
       mbar_wait(&pv_done[j], (blk_it - 1) & 1);
-      if (lane == 0 && (warp & 3) == 0) att_trace(EV_ODONE, k, 0, j);
+      if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_ODONE, k, 0, j);
       ++u_it;
       tc_fence_after();
       const float inv = 1.f / l_run;
@@ -428,7 +442,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           tma_store_commit();
         }
       }
-      if (lane == 0 && (warp & 3) == 0) att_trace(EV_EPI_DONE, k, 0, j);
+      if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_EPI_DONE, k, 0, j);
       tc_fence_before();
     }
   }
@@ -443,12 +457,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 int debug_set_attention_trace(unsigned long long* buf, unsigned int cap) {
-  unsigned int zero = 0;
-  cudaMemcpyToSymbol(g_att_trace, &buf, sizeof(buf));
-  cudaMemcpyToSymbol(g_att_trace_n, &zero, sizeof(zero));
-  cudaMemcpyToSymbol(g_att_trace_cap, &cap, sizeof(cap));
-  cudaError_t e = cudaDeviceSynchronize();
-  return e == cudaSuccess ? 0 : fail(-4, "trace setup: %s", cudaGetErrorString(e));
+  g_trace_buf = buf;
+  g_trace_cap = buf == nullptr ? 0 : cap;
+  return 0;
 }
 
 static int g_att_sms = 0;
@@ -484,7 +495,10 @@ static int launch_attention_t(const AttnDesc& d, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_prefix_kernel<DH>, tq, tkv, to, d, n_units);
+  AttnDesc dd = d;
+  dd.trace = g_trace_buf;
+  dd.trace_cap = g_trace_cap;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_prefix_kernel<DH>, tq, tkv, to, dd, n_units);
   if (e != cudaSuccess) return fail(-4, "attention launch: %s", cudaGetErrorString(e));
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(-4, "attention launch: %s", cudaGetErrorString(e));

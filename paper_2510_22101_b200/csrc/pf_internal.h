@@ -93,6 +93,8 @@ struct AttnDesc {
   int n_work;
   const int32_t* segs;    // [n_seg x 4] : {prefix_off, P, suffix_off, S}  (prefix segment: S=0)
   float scale;
+  unsigned long long* trace;   // debug event trace (pf_debug_set_trace), normally null
+  unsigned int trace_cap;
 };
 int launch_attention(const AttnDesc& d, cudaStream_t stream);
 int debug_set_attention_trace(unsigned long long* buf, unsigned int cap);
