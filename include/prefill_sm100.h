@@ -135,6 +135,7 @@ typedef struct pf_gemm_args {
   int M, N, K, epilogue;
   const int32_t* pos; const float* rope_cos; const float* rope_sin; int rope_heads; int rope_dh;
   const float* row_ss; long long ss_ld; float* ss_out; void* xb; int ldxb; float inv_d, eps;
+  const float* rope_cs;  /* optional: per-row cos/sin pre-gathered in the QKV epilogue's coalesced layout */
 } pf_gemm_args;
 PF_API int pf_gemm_bf16_ex(const pf_gemm_args* args, pf_stream_t stream);
 /* Embedding gather; every output is optional (NULL skips it): resid = float(E[ids]) (fp32),

@@ -68,6 +68,7 @@ class PfGemmArgs(ctypes.Structure):
         ("rope_heads", ctypes.c_int), ("rope_dh", ctypes.c_int),
         ("row_ss", ctypes.c_void_p), ("ss_ld", ctypes.c_longlong), ("ss_out", ctypes.c_void_p),
         ("xb", ctypes.c_void_p), ("ldxb", ctypes.c_int), ("inv_d", ctypes.c_float), ("eps", ctypes.c_float),
+        ("rope_cs", ctypes.c_void_p),
     ]
 
 

@@ -409,6 +409,7 @@ int pf_gemm_bf16_ex(const pf_gemm_args* a, pf_stream_t stream) {
   g.rope_dh = a->rope_dh;
   g.row_ss = a->row_ss; g.ss_ld = a->ss_ld; g.ss_out = a->ss_out; g.xb = a->xb; g.ldxb = a->ldxb;
   g.inv_d = a->inv_d; g.eps = a->eps;
+  g.rope_cs = a->rope_cs;
   return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -51,9 +51,11 @@ struct GemmCfg {
   static constexpr int B_BYTES = B_ROWS * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
   static constexpr bool RING = EPI == EPI_RESID_ADD_NORM;
-  static constexpr int STAGES = RING ? PF_RING_STAGES : (CG == 2 ? 6 : 4);
-  // ring: RB_DEPTH (hi, lo) chunk slots per epilogue warp; otherwise 2 staging boxes per warp
-  static constexpr int EPI_BYTES = RING ? 4 * RB_DEPTH * RB_SLOT : 4 * 2 * GEMM_STG_BYTES;
+  static constexpr bool ROPE = EPI == EPI_ROPE_BF16;
+  // the RoPE epilogue stages a whole 256-column tile (4 boxes per warp) and gives up a stage for it
+  static constexpr int STAGES = RING ? PF_RING_STAGES : ROPE ? (CG == 2 ? 5 : 3) : (CG == 2 ? 6 : 4);
+  // ring: RB_DEPTH (hi, lo) chunk slots per epilogue warp; otherwise 2 (RoPE: 4) staging boxes per warp
+  static constexpr int EPI_BYTES = RING ? 4 * RB_DEPTH * RB_SLOT : 4 * (ROPE ? 4 : 2) * GEMM_STG_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
   static constexpr int TILE_M = GEMM_BM * CG;
 };
@@ -282,6 +284,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * GEMM_BN;
+      // Hand the accumulator buffer back to the MMA issuer (its tcgen05.ld reads are complete).
+      auto release_acc = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          // the MMA issuer waits on the leader CTA's tmem-empty barrier
+          if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+          else mbar_arrive_relaxed(&tempty_bar[acc]);
+        }
+      };
       const int grow = m0 + (int)row;
       const bool rvalid = grow < args.M;
       // fused RMSNorm: the A rows were bf16(residual); scale the accumulator row by rstd
@@ -416,16 +428,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       } else {  // EPI_ROPE_BF16
         // Rotate-half RoPE on heads of width dh (64 or 128): head column e pairs with e + dh/2.
-        // Work item i = (head hd, 32-column block c of the first half): x1 = cols [32c, 32c+32),
-        // x2 = cols [dh/2 + 32c, ...).  Items are software-pipelined: item i+1's tcgen05.ld is in
-        // flight during item i's math, cos/sin loads are issued before the TMEM wait, and the wait
-        // for the staging buffer (previous head's TMA store) comes after the math.  Outputs land in
-        // 64-column SW128 boxes: dh=128 -> 2 boxes per head (single-buffered), dh=64 -> 1 box per
-        // head (double-buffered across heads).
+        // Work item = (32-column block c of the head half, head hd): x1 = cols [32c, 32c+32) and
+        // x2 = cols [dh/2 + 32c, ...) of head hd.  c is the outer loop, so each row's cos/sin block
+        // is loaded once and serves every head of the tile (dh=128: 2 heads, dh=64: 4).  Items are
+        // software-pipelined (item i+1's tcgen05.ld in flight during item i's math); the whole
+        // 256-column tile is staged in 4 SW128 boxes per warp and leaves by TMA after the last item,
+        // so the only staging wait is for the previous tile's stores (issued a mainloop earlier).
         const int dh = args.rope_dh;
         const int half = dh / 2;
         const int cpb = half / 32;                    // 32-col blocks per head half (1 or 2)
-        const int n_items = GEMM_BN / 32 / 2;         // 4 for both head widths
+        const int hpt = GEMM_BN / dh;                 // heads per tile (2 or 4)
+        const int n_items = cpb * hpt;                // 4 for both head widths
         const int p = rvalid ? __ldg(args.pos + grow) : 0;
         // cos/sin of this row: gathered layout (coalesced: quad q of the warp's 32 rows is 512
         // contiguous bytes, stride 32 float4) or the tables' row p (32 lines per warp load)
@@ -443,22 +456,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
           qstride = 1;
         }
+        const bool row_rot = r0 < args.M;   // rows past M are padding (the gathered table ends there)
         const uint32_t stg0 = smem_u32(my_stg);
         uint32_t x1[32], x2[32];
         tmem_ld_32x32b_x32(t_row, x1);
         tmem_ld_32x32b_x32(t_row + half, x2);
+        float4 cv[8], sv[8];
 #pragma unroll 1
         for (int it = 0; it < n_items; ++it) {
-          const int hd = it / cpb, c = it % cpb;
-          // rows past M are padding: skip the rotation (the gathered table ends at ceil(M/32) groups)
-          const bool rot = ((n0 + hd * dh) / dh) < args.rope_heads && r0 < args.M;
-          float4 cv[8], sv[8];
+          const int c = it / hpt, hd = it % hpt;
+          if (hd == 0) {
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            cv[j4] = rot ? __ldg(cs4 + (c * 8 + j4) * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
-            sv[j4] = rot ? __ldg(sn4 + (c * 8 + j4) * qstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j4 = 0; j4 < 8; ++j4) {
+              cv[j4] = row_rot ? __ldg(cs4 + (c * 8 + j4) * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
+              sv[j4] = row_rot ? __ldg(sn4 + (c * 8 + j4) * qstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
           }
+          const bool rot = ((n0 + hd * dh) / dh) < args.rope_heads;   // q and k heads; v passes through
           tmem_ld_wait();
+          if (it == n_items - 1) release_acc();   // last TMEM read done: the MMA may reuse the buffer
           uint32_t w1[16], w2[16];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
@@ -469,8 +485,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int e = 0; e < 4; ++e) {
               const float a = __uint_as_float(x1[j4 * 4 + e]) * rs;
               const float b = __uint_as_float(x2[j4 * 4 + e]) * rs;
-              o1[e] = a * cc[e] - b * ss[e];
-              o2[e] = b * cc[e] + a * ss[e];
+              o1[e] = rot ? a * cc[e] - b * ss[e] : a;
+              o2[e] = rot ? b * cc[e] + a * ss[e] : b;
             }
             w1[j4 * 2] = pack_bf16x2(o1[0], o1[1]);
             w1[j4 * 2 + 1] = pack_bf16x2(o1[2], o1[3]);
@@ -478,47 +494,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             w2[j4 * 2 + 1] = pack_bf16x2(o2[2], o2[3]);
           }
           if (it + 1 < n_items) {
-            const int hn = (it + 1) / cpb, cn = (it + 1) % cpb;
+            const int cn = (it + 1) / hpt, hn = (it + 1) % hpt;
             tmem_ld_32x32b_x32(t_row + hn * dh + cn * 32, x1);
             tmem_ld_32x32b_x32(t_row + hn * dh + half + cn * 32, x2);
           }
-          // staging boxes of this head: dh=128 -> boxes {0,1}; dh=64 -> box hd&1
-          const uint32_t hbase = stg0 + (dh == 64 ? (hd & 1) : 0) * GEMM_STG_BYTES;
-          if (c == 0) {
-            if (lane == 0) {
-              if (dh == 64) tma_store_wait_read<1>(); else tma_store_wait_read<0>();
-            }
+          if (it == 0) {   // previous tile's boxes have been read by their TMA stores
+            if (lane == 0) tma_store_wait_read<0>();
             __syncwarp();
           }
-          const int e1 = c * 32, e2 = half + c * 32;   // head-local first column of each part
-          const uint32_t b1 = hbase + (e1 / 64) * GEMM_STG_BYTES + lane * 128;
-          const uint32_t b2 = hbase + (e2 / 64) * GEMM_STG_BYTES + lane * 128;
+          const int e1 = hd * dh + c * 32, e2 = hd * dh + half + c * 32;   // tile column of each part
+          const uint32_t b1 = stg0 + (e1 / 64) * GEMM_STG_BYTES + lane * 128;
+          const uint32_t b2 = stg0 + (e2 / 64) * GEMM_STG_BYTES + lane * 128;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             const uint32_t k1 = (e1 % 64) / 8 + q4, k2 = (e2 % 64) / 8 + q4;
             st_shared_v4(b1 + ((k1 ^ (lane & 7)) << 4), w1[4 * q4], w1[4 * q4 + 1], w1[4 * q4 + 2], w1[4 * q4 + 3]);
             st_shared_v4(b2 + ((k2 ^ (lane & 7)) << 4), w2[4 * q4], w2[4 * q4 + 1], w2[4 * q4 + 2], w2[4 * q4 + 3]);
           }
-          if (c == cpb - 1) {
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              const uint8_t* hb = my_stg + (dh == 64 ? (hd & 1) : 0) * GEMM_STG_BYTES;
-              for (int x = 0; x < dh / 64; ++x)
-                tma_store_2d(&tmC, hb + x * GEMM_STG_BYTES, n0 + hd * dh + 64 * x, r0);
-              tma_store_commit();
-            }
-          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          for (int x = 0; x < GEMM_BN / 64; ++x)
+            if (n0 + 64 * x < args.N) tma_store_2d(&tmC, my_stg + x * GEMM_STG_BYTES, n0 + 64 * x, r0);
+          tma_store_commit();
         }
       }
       // All TMEM reads of this accumulator are complete (tcgen05.wait::ld above).
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        // the MMA issuer waits on the leader CTA's tmem-empty barrier
-        if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
-        else mbar_arrive_relaxed(&tempty_bar[acc]);
-      }
+      if constexpr (EPI != EPI_ROPE_BF16) release_acc();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) tma_store_wait_all<0>();

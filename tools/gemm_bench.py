@@ -25,6 +25,7 @@ SHAPES = [  # name, M, N (B rows), K, epilogue, useful flops (true widths)
     ("C2 o+resid+norm", T2, 1024, 2048, _lib.EPI_RESID_ADD_NORM, 2 * T2 * 1024 * 2048),
     ("qkv+rope", T, 2560, 2048, _lib.EPI_ROPE_BF16, 2 * T * 2560 * 2048),
     ("qkv plain", T, 2560, 2048, _lib.EPI_BF16, 2 * T * 2560 * 2048),
+    ("C2 qkv plain", T2, 4096, 1024, _lib.EPI_BF16, 2 * T2 * 4096 * 1024),
     ("o plain", T, 2048, 1280, _lib.EPI_BF16, 2 * T * 2048 * 1280),
     ("down plain", T, 2048, 3712, _lib.EPI_BF16, 2 * T * 3686 * 2048),
     ("o+resid", T, 2048, 1280, _lib.EPI_RESID_ADD, 2 * T * 2048 * 1280),
@@ -71,12 +72,15 @@ def main():
 
         xb = torch.empty(M, ncol, device="cuda", dtype=torch.bfloat16) if epi == _lib.EPI_RESID_ADD_NORM else None
         ss = torch.ones(32, M, device="cuda")   # partial sums [part][M]
+        # gathered cos/sin in the epilogue's layout (as pf_score builds it with rope_gather_kernel)
+        cs_g = torch.rand(((M + 31) // 32) * 32 * 2 * 64, device="cuda")
         args = _lib.PfGemmArgs(A=A.data_ptr(), lda=K, B=B.data_ptr(), ldb=K, C=C.data_ptr(), ldc=ncol, M=M, N=N,
                                K=K, epilogue=epi, pos=pos.data_ptr() if epi == 1 else None,
                                rope_cos=cos.data_ptr(), rope_sin=sin.data_ptr(), rope_heads=(N // 128) * 3 // 4 if epi == 1 else 0,
                                row_ss=ss.data_ptr() if epi in (1, 2) else None,
                                ss_out=ss.data_ptr() if xb is not None else None,
-                               xb=xb.data_ptr() if xb is not None else None, ldxb=ncol, inv_d=1.0 / K, eps=1e-6)
+                               xb=xb.data_ptr() if xb is not None else None, ldxb=ncol, inv_d=1.0 / K, eps=1e-6,
+                               rope_cs=cs_g.data_ptr() if epi == 1 else None)
 
         def ours():
             _lib.check(lib.pf_gemm_bf16_ex(ctypes.byref(args), stream))
