@@ -29,7 +29,7 @@ def main():
     for _ in range(a.warmup + a.steps):
         scorer.score_device(dp)
     torch.cuda.synchronize()
-    print("launches per step:", 2 + 7 * cfg.n_layers)
+    print("launches per step:", 5 * cfg.n_layers + 4)
 
 
 if __name__ == "__main__":
