@@ -273,3 +273,58 @@ def test_gemm_rope_dh64(lib):
             pos=pos, rope_cos=cos, rope_sin=sin, rope_heads=H + Hkv, rope_dh=64)
     ref = rope_ref(A.float() @ B.float().t(), pos, cos, sin, H + Hkv, dh=64)
     torch.testing.assert_close(C.float(), ref, rtol=1.6e-2, atol=2e-2)
+
+
+def gathered_cos_sin(cos, sin, pos):
+    """The QKV epilogue's pre-gathered layout (elementwise.cu rope_gather_kernel): per 32-row group
+    g, [cos | sin] x [half/4 float4 chunks] x [32 rows] x float4, so a warp's loads are coalesced."""
+    T, half = pos.numel(), cos.shape[1]
+    G, qn = (T + 31) // 32, half // 4
+    cs = torch.zeros(G * 32, 2, qn, 4, device="cuda")
+    cs[:T, 0] = cos[pos.long()].view(T, qn, 4)
+    cs[:T, 1] = sin[pos.long()].view(T, qn, 4)
+    return cs.view(G, 32, 2, qn, 4).permute(0, 2, 3, 1, 4).contiguous()
+
+
+@pytest.mark.parametrize("M,H,Hkv,K,dh", [(1000, 10, 5, 512, 128), (777, 4, 2, 256, 64)])
+def test_gemm_rope_gathered_table(lib, M, H, Hkv, K, dh):
+    """RoPE epilogue reading the gathered cos/sin rows (the layout pf_score uses), including a ragged
+    last 32-row group and V heads that pass through unrotated."""
+    cfg = ModelConfig(n_layers=1, d_model=K, n_heads=H, n_kv_heads=Hkv, d_ff=128, d_head=dh)
+    cos, sin = (torch.from_numpy(t).cuda() for t in rope_tables(cfg))
+    N = (H + 2 * Hkv) * dh
+    A = rand_bf16(M, K, seed=50)
+    B = rand_bf16(N, K, scale=K ** -0.5, seed=51)
+    pos = torch.randint(0, cfg.max_seq, (M,), device="cuda", dtype=torch.int32)
+    cs = gathered_cos_sin(cos, sin, pos)
+    C = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    gemm_ex(lib, A=A, lda=K, B=B, ldb=K, C=C, ldc=N, M=M, N=N, K=K, epilogue=_lib.EPI_ROPE_BF16,
+            pos=pos, rope_cos=cos, rope_sin=sin, rope_heads=H + Hkv, rope_dh=dh, rope_cs=cs)
+    ref = rope_ref(A.float() @ B.float().t(), pos, cos, sin, H + Hkv, dh=dh)
+    torch.testing.assert_close(C.float(), ref, rtol=1.6e-2, atol=2e-2)
+
+
+def test_prefix_attention_rescales_and_masked_blocks(lib):
+    """Online softmax under large score swings (the lazy rescale of O in TMEM fires when the running
+    max grows by > 2^8) and items long enough that whole warps see fully masked 32-key halves."""
+    H, Hkv, dh = 4, 2, 128
+    rng = np.random.default_rng(3)
+    reqs = [SharedBatch(list(rng.integers(16, 100, 64)), [list(rng.integers(16, 100, s)) for s in (250, 129, 64)]),
+            SharedBatch([], [list(rng.integers(16, 100, 190))])]
+    packed = pack_requests(reqs)
+    T = packed.T
+    g = torch.Generator(device="cuda").manual_seed(7)
+    qkv = torch.randn(T, (H + 2 * Hkv) * dh, device="cuda", generator=g)
+    # keys grow with the row index: every later block raises the row max far past the threshold
+    k0 = H * dh
+    qkv[:, k0:k0 + Hkv * dh] *= torch.linspace(0.5, 6.0, T, device="cuda")[:, None]
+    qkv[:, :H * dh] *= 3.0
+    qkv = qkv.to(torch.bfloat16)
+    out = torch.full((T, H * dh), float("nan"), device="cuda", dtype=torch.bfloat16)
+    segs = torch.from_numpy(packed.segs).cuda()
+    work = torch.from_numpy(packed.work).cuda()
+    _lib.check(lib.pf_prefix_attention(P(qkv), P(out), T, H, Hkv, dh, P(segs), P(work), len(packed.work), stream()))
+    torch.cuda.synchronize()
+    ref = attention_ref(qkv, packed, H, Hkv, dh)
+    assert torch.isfinite(out.float()).all()
+    torch.testing.assert_close(out.float(), ref, rtol=2e-2, atol=3e-2)
