@@ -19,7 +19,11 @@ What it restates (all citations into /root/reference):
   "parity unpinned" by reference-executed outputs.  It is pinned by the spec's known-answer
   examples and invariants (tests/test_oracle.py) and the token-id / prompt-structure golden
   vectors generated from the importable reference tokenizer.py + corpus.py
-  (tests/golden/make_golden.py).
+  (tests/golden/make_golden.py).  Its transformer arithmetic is additionally pinned against an
+  independent implementation: Hugging Face transformers' LlamaForCausalLM in float64 on the same
+  weights agrees to ~1e-14 on last-token logits (tests/golden/make_hf_llama_golden.py ->
+  hf_llama_logits.json; tests/test_oracle_hf.py), for the C1 shape, a GQA model with
+  n_heads*d_head != d_model and a 10/5-head pruned shape, including the prefix-shared path.
 
 Open choices the spec leaves (pinned identically in the product): pre-norm blocks,
 RMSNorm eps 1e-6, rotate-half RoPE with theta^(-2i/d_head) tables computed in float64, GQA head

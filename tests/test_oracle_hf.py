@@ -1,0 +1,80 @@
+"""The oracle's transformer arithmetic against an independent implementation (CPU only).
+
+The reference ships no model code, so its logits cannot pin the oracle.  These
+tests pin it against Hugging Face transformers' LlamaForCausalLM run in float64 on the same weights:
+golden vectors committed in tests/golden/hf_llama_logits.json (generator:
+tests/golden/make_hf_llama_golden.py), plus one live HF comparison when transformers is importable.
+Measured agreement is ~1e-14 in float64; the gate here is 1e-9.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle.model as OM
+import oracle.prefixcache as OP
+from tests.golden import make_hf_llama_golden as G
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hf_llama_logits.json")))
+RECORDS = GOLD["records"]
+TOL64 = 1e-9
+
+
+def _weights(name, cache={}):
+    if name not in cache:
+        cfg, W, _ = G.build_weights(name)
+        cache[name] = (cfg, W, W.astype(np.float64))
+    return cache[name]
+
+
+def _check(logits, r, tol, rel=0.0):
+    idx = np.asarray(r["sample_idx"])
+    scale = 1.0 + rel * np.abs(np.asarray(r["sample"]))
+    assert np.all(np.abs(logits[idx] - np.asarray(r["sample"])) <= tol * scale)
+    assert abs(logits[1] - r["yes"]) <= tol * (1 + rel * abs(r["yes"]))
+    assert abs(logits[2] - r["no"]) <= tol * (1 + rel * abs(r["no"]))
+    n = logits.size
+    assert abs(logits.sum() - r["sum"]) <= tol * n ** 0.5 * 10
+    assert abs((logits * logits).sum() - r["sumsq"]) <= tol * 10 * max(1.0, r["sumsq"]) ** 0.5 * n ** 0.5
+
+
+@pytest.mark.parametrize("i", range(len(RECORDS)), ids=[f"{r['config']}-S{len(r['tokens'])}" for r in RECORDS])
+def test_oracle_f64_matches_hf_llama(i):
+    r = RECORDS[i]
+    _, _, W64 = _weights(r["config"])
+    logits, _ = OM.forward_prefill(W64, r["tokens"])
+    _check(logits, r, TOL64)
+
+
+@pytest.mark.parametrize("i", [i for i, r in enumerate(RECORDS) if len(r["tokens"]) == 300])
+def test_oracle_f32_close_to_hf_llama(i):
+    r = RECORDS[i]
+    _, W32, _ = _weights(r["config"])
+    logits, _ = OM.forward_prefill(W32, r["tokens"])
+    _check(logits.astype(np.float64), r, 2e-3, rel=1e-3)
+
+
+@pytest.mark.parametrize("i", [i for i, r in enumerate(RECORDS) if len(r["tokens"]) >= 37])
+def test_shared_prefix_scoring_matches_hf_full_sequence(i):
+    """The reference's prefix-sharing contract: prefix KV once, suffix
+    positions continuing at P, LSE-merged attention = HF's plain causal pass over the whole prompt."""
+    r = RECORDS[i]
+    _, _, W64 = _weights(r["config"])
+    toks = r["tokens"]
+    P = len(toks) // 3
+    logits = OP.score_shared_batch(W64, OP.SharedBatch(toks[:P], [toks[P:]]))[0]
+    _check(np.asarray(logits), r, TOL64)
+
+
+def test_live_hf_llama_new_sequence():
+    """A sequence not in the fixture, HF run live (skips if transformers is absent)."""
+    pytest.importorskip("transformers")
+    cfg, W, _ = G.build_weights("GQA_DH128")
+    m = G.hf_model(cfg, W)
+    rng = np.random.default_rng(99)
+    toks = [3] + [int(x) for x in rng.integers(16, cfg.vocab_size, 90)] + [11]
+    ref = G.hf_last_logits(m, toks)
+    mine, _ = OM.forward_prefill(W.astype(np.float64), toks)
+    assert float(np.max(np.abs(mine - ref))) < TOL64
