@@ -32,7 +32,7 @@ OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "hf_llama_logits.
 # (name, n_layers, d_model, n_heads, n_kv_heads, d_head, d_ff): C1 (BASELINE configs[0] shape),
 # a GQA model with n_heads*d_head != d_model, and a C4-like pruned head/FFN ratio (10/5 heads).
 CONFIGS = [("C1", 2, 256, 4, 2, 64, 1024), ("GQA_DH128", 3, 384, 4, 2, 128, 600),
-           ("PRUNED_10_5", 2, 320, 10, 5, 128, 370)]
+           ("PRUNED_10_5", 2, 640, 10, 5, 128, 370)]
 SEQ_LENS = (1, 37, 300)
 SAMPLE = np.linspace(0, 32767, 256).astype(np.int64)
 

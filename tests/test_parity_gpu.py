@@ -326,3 +326,35 @@ def test_c3_width_long_items():
     dp = np.abs(res.p_yes - p_ref)
     print(f"C3-width long items: max|dp|={dp.max():.2e}")
     assert dp.max() <= TOL_P
+
+
+@pytest.mark.parametrize("name", ["C1", "GQA_DH128", "PRUNED_10_5"])
+def test_gpu_matches_hf_llama_golden(name):
+    """The device path against the independent float64 reference (HF LlamaForCausalLM on the same
+    weights, tests/golden/hf_llama_logits.json): p_yes within the north_star tolerance, for the
+    1/37/300-token golden prompts scored as one-item shared-prefix requests."""
+    import json
+    import os
+
+    from paper_2510_22101_b200 import ModelConfig, split_shared_prefix
+    from tests.golden import make_hf_llama_golden as G
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hf_llama_logits.json")))
+    recs = [r for r in gold["records"] if r["config"] == name]
+    L, d, H, Hkv, dh, f = recs[0]["dims"]
+    cfg = ModelConfig(n_layers=L, d_model=d, n_heads=H, n_kv_heads=Hkv, d_ff=f, d_head=dh, vocab_size=32768)
+    _, ow, _ = G.build_weights(name)
+    w = init_weights(cfg, 3)   # same values as the oracle's init (seed 3); gains from the fixture's draw
+    for lw, olw in zip(w.layers, ow.layers):
+        assert np.array_equal(lw.W_q, olw["W_q"]) and np.array_equal(lw.W_down, olw["W_down"])
+        lw.rms_attn, lw.rms_mlp = olw["rms_attn"], olw["rms_mlp"]
+    w.final_norm = ow.final_norm
+    scorer = PrefillScorer(w)
+    dp_max = dl_max = 0.0
+    for r in recs:
+        res = score_shared_batch(scorer, split_shared_prefix([r["tokens"]]))
+        p_ref = 1.0 / (1.0 + np.exp(-(r["yes"] - r["no"])))
+        dp_max = max(dp_max, abs(float(res.p_yes[0]) - p_ref))
+        dl_max = max(dl_max, float(np.max(np.abs(res.logits2[0] - [r["yes"], r["no"]]))))
+    print(f"{name}: max |dp| vs HF Llama f64 = {dp_max:.2e}, max |dlogit| = {dl_max:.2e}")
+    assert dp_max <= TOL_P
