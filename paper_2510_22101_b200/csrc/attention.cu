@@ -506,6 +506,9 @@ static int launch_attention_t(const AttnDesc& d, cudaStream_t stream) {
 }
 
 int launch_attention(const AttnDesc& d, cudaStream_t stream) {
+#ifdef PF_DEBUG_SKIP_ATTENTION   // A/B builds only (tools/build_variant.sh): the step without attention
+  return 0;
+#endif
   if (d.dh != 128 && d.dh != 64) return fail(-2, "attention: d_head must be 64 or 128 (got %d)", d.dh);
   if (d.H % d.Hkv != 0) return fail(-2, "attention: n_heads %% n_kv_heads != 0");
   if (d.n_work == 0) return 0;

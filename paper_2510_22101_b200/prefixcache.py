@@ -162,7 +162,7 @@ def pack_requests(batches: Sequence[SharedBatch], max_seq: int = 2048) -> Packed
 
 def make_work(segs: np.ndarray) -> np.ndarray:
     """One work entry per 128-row query tile; heaviest tiles (most key blocks) first so the
-    longest CTAs start in the first wave."""
+    longest CTAs start in the first wave, ties in descending segment order (L2 reuse, below)."""
     q_len = segs[:, 3].astype(np.int64)
     kv_len = segs[:, 1].astype(np.int64)
     ntile = (q_len + ATTN_TILE - 1) // ATTN_TILE
@@ -170,7 +170,9 @@ def make_work(segs: np.ndarray) -> np.ndarray:
     starts = np.cumsum(ntile) - ntile
     tile = np.arange(int(ntile.sum()), dtype=np.int64) - np.repeat(starts, ntile)
     cost = (kv_len[seg_idx] + ATTN_TILE - 1) // ATTN_TILE + tile + 1
-    order = np.lexsort((tile, seg_idx, -cost))
+    # equal-cost tiles in descending row order: the QKV GEMM writes rows in ascending order, so the
+    # first attention units read the rows it wrote last, while they are still in L2
+    order = np.lexsort((tile, -seg_idx, -cost))
     work = np.zeros((len(seg_idx), 4), dtype=np.int32)
     work[:, 0] = seg_idx[order]
     work[:, 1] = tile[order]

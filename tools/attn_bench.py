@@ -48,7 +48,12 @@ def main():
         qkv = (torch.randn(T, (H + 2 * Hkv) * dh, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
         out = torch.zeros(T, H * dh, device="cuda", dtype=torch.bfloat16)
         segs = torch.from_numpy(packed.segs).cuda()
-        work = torch.from_numpy(packed.work).cuda()
+        wk = packed.work.copy()
+        if os.environ.get("PF_ATTN_L2") == "1":
+            # timing probe: every work tile re-reads one of 16 items (footprint L2-resident)
+            items = wk[:, 0] != 0
+            wk[items, 0] = 1 + (wk[items, 0] - 1) % 16
+        work = torch.from_numpy(wk).cuda()
         st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         P = lambda t: ctypes.c_void_p(t.data_ptr())
         run = lambda: _lib.check(lib.pf_prefix_attention(P(qkv), P(out), T, H, Hkv, dh, P(segs), P(work),
