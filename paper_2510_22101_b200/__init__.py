@@ -9,14 +9,14 @@ runs in libprefill_sm100.so (hand-written tcgen05/TMA kernels) behind a C-ABI.
 
 from .calibration import CalibrationSet, capture_calibration, prune_mlp_neurons_calibrated, sample_positions
 from .config import CONFIGS, REQUESTS, ModelConfig, RequestShape
-from .prefixcache import (AttentionPartial, PackedBatch, SharedBatch, merge_attention,
+from .prefixcache import (AttentionPartial, PackedBatch, SharedBatch, concat_packed, merge_attention,
                           pack_requests, pack_token_lists, split_shared_prefix, throughput_gain)
 from .scoring import RankedList, RelevanceScore, rank_items, relevance_score, top_k
 from .weights import DeviceWeights, Weights, init_device_weights, init_weights, to_device
 
 __all__ = [
     "CONFIGS", "REQUESTS", "ModelConfig", "RequestShape", "AttentionPartial", "PackedBatch",
-    "SharedBatch", "merge_attention", "pack_requests", "pack_token_lists", "split_shared_prefix",
+    "SharedBatch", "concat_packed", "merge_attention", "pack_requests", "pack_token_lists", "split_shared_prefix",
     "throughput_gain", "RankedList", "RelevanceScore", "rank_items", "relevance_score", "top_k",
     "DeviceWeights", "Weights", "init_device_weights", "init_weights", "to_device",
     "PrefillScorer", "score_shared_batch",

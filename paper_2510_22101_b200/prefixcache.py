@@ -160,6 +160,29 @@ def pack_requests(batches: Sequence[SharedBatch], max_seq: int = 2048) -> Packed
     )
 
 
+def concat_packed(parts: Sequence[PackedBatch]) -> PackedBatch:
+    """Join requests packed separately (e.g. at arrival, off the serving loop) into one launch.
+    Row offsets in segs / last_idx shift by the preceding parts' T, request indices by their request
+    counts, and the work list is rebuilt over the joined segments; the result equals
+    ``pack_requests`` over the concatenated request list, array for array."""
+    if len(parts) == 0:
+        raise ValueError("concat_packed: no requests")
+    if len(parts) == 1:
+        return parts[0]
+    t_off = np.cumsum([0] + [p.T for p in parts[:-1]]).astype(np.int32)
+    r_off = np.cumsum([0] + [len(p.prefix_lens) for p in parts[:-1]]).astype(np.int32)
+    segs = np.concatenate([p.segs + np.array([o, 0, o, 0], dtype=np.int32) for p, o in zip(parts, t_off)])
+    return PackedBatch(
+        ids=np.concatenate([p.ids for p in parts]),
+        pos=np.concatenate([p.pos for p in parts]),
+        segs=segs, work=make_work(segs),
+        last_idx=np.concatenate([p.last_idx + o for p, o in zip(parts, t_off)]).astype(np.int32),
+        item_request=np.concatenate([p.item_request + o for p, o in zip(parts, r_off)]).astype(np.int32),
+        prefix_lens=np.concatenate([p.prefix_lens for p in parts]),
+        suffix_lens=np.concatenate([p.suffix_lens for p in parts]),
+    )
+
+
 def make_work(segs: np.ndarray) -> np.ndarray:
     """One work entry per 128-row query tile; heaviest tiles (most key blocks) first so the
     longest CTAs start in the first wave, ties in descending segment order (L2 reuse, below)."""

@@ -116,3 +116,21 @@ def test_throughput_gain_and_merge_product():
                                                   OM.AttentionPartial(b.output, b.lse)), atol=1e-12)
     c = PC.merge_attention(PC.AttentionPartial(a.output, np.full((2, 3), -np.inf)), b)
     np.testing.assert_array_equal(c, b.output)
+
+
+def test_concat_packed_equals_joint_packing():
+    """Requests packed one by one (at arrival) and joined per launch give the same arrays as
+    packing the whole batch at once: segments, work order, last rows, request ids."""
+    from paper_2510_22101_b200 import SharedBatch, concat_packed, pack_requests
+
+    rng = np.random.default_rng(21)
+    reqs = []
+    for _ in range(5):
+        P = int(rng.integers(0, 80))
+        sufs = [list(rng.integers(16, 1000, int(rng.integers(1, 300)))) for _ in range(int(rng.integers(1, 9)))]
+        reqs.append(SharedBatch(list(rng.integers(16, 1000, P)), sufs))
+    joint = pack_requests(reqs)
+    joined = concat_packed([pack_requests([r]) for r in reqs])
+    for f in ("ids", "pos", "segs", "work", "last_idx", "item_request", "prefix_lens", "suffix_lens"):
+        a, b = getattr(joint, f), getattr(joined, f)
+        assert a.dtype == b.dtype and np.array_equal(a, b), f
