@@ -468,7 +468,7 @@ def main():
     ap.add_argument("--load-token-budget", type=int, default=262144)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-items", type=int, default=2)
+    ap.add_argument("--ref-items", type=int, default=8, help="items per reference step (one shared prefix per step)")
     ap.add_argument("--no-graph", action="store_true", help="launch pf_score directly instead of graph replay")
     args = ap.parse_args()
     if args.impl == "reference":
