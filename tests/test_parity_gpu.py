@@ -358,3 +358,28 @@ def test_gpu_matches_hf_llama_golden(name):
         dl_max = max(dl_max, float(np.max(np.abs(res.logits2[0] - [r["yes"], r["no"]]))))
     print(f"{name}: max |dp| vs HF Llama f64 = {dp_max:.2e}, max |dlogit| = {dl_max:.2e}")
     assert dp_max <= TOL_P
+
+
+@pytest.mark.slow
+def test_full_size_properties_bit_exact():
+    """BASELINE C4 at full size (28 layers, 64-token prefix + 256 items x 100 tokens), checked through
+    properties that need no oracle at this size.  Every row's arithmetic is independent of the
+    other rows (per-row K accumulation order, per-row norm partials summed in a fixed order), so:
+      * reversing the item order reverses the scores bit for bit;
+      * the same items split into 4 requests that each carry their own copy of the prefix score
+        bit-identically to the single shared-prefix request (prefix sharing is exact)."""
+    from paper_2510_22101_b200 import REQUESTS, SharedBatch, init_device_weights
+
+    cfg, shape = CONFIGS["C4"], REQUESTS["C4"]
+    scorer = PrefillScorer(init_device_weights(cfg, 0, "cuda"))
+    rng = np.random.default_rng(17)
+    sb = make_shared(rng, shape.prefix_len, [shape.suffix_len] * shape.n_items, "spread")
+    base = scorer.score_packed(pack_requests([sb]))
+    rev = scorer.score_packed(pack_requests([SharedBatch(sb.prefix_tokens, sb.suffixes[::-1])]))
+    np.testing.assert_array_equal(rev.p_yes[::-1], base.p_yes)
+    np.testing.assert_array_equal(rev.logits2[::-1], base.logits2)
+    q = shape.n_items // 4
+    split = [SharedBatch(list(sb.prefix_tokens), sb.suffixes[i * q:(i + 1) * q]) for i in range(4)]
+    sp = scorer.score_packed(pack_requests(split))
+    np.testing.assert_array_equal(sp.p_yes, base.p_yes)
+    np.testing.assert_array_equal(sp.logits2, base.logits2)
