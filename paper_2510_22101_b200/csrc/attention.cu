@@ -74,6 +74,44 @@ PF_DEVICE void att_trace(const AttnDesc& d, int ev, int unit, int blk, int who) 
                    (globaltimer_ns() & 0xffffffffull);
 }
 
+// Cycle accounting of the softmax warps (debug, with the trace buffer): per-phase clock64 sums,
+// accumulated by lane 0 of every softmax warp into the last 64 slots of the trace buffer:
+// [0] s_full wait, [1] softmax math (S load -> P store issued), [2] pv_done wait, [3] rescale,
+// [4] P store wait + p_ready, [5] o_done/pv_done wait before the epilogue, [6] epilogue, [7] units.
+enum AttPhase { PH_SWAIT, PH_MATH, PH_PVWAIT, PH_RESCALE, PH_ARRIVE, PH_ODONE, PH_EPI, PH_UNITS,
+                PH_EPI_WAIT, PH_EPI_LD, PH_EPI_CVT, PH_N };
+#ifdef PF_ATT_PHASES   // A/B builds only (tools/build_variant.sh NAME -DPF_ATT_PHASES)
+struct PhaseClock {
+  long long acc[PH_N];
+  long long t;
+  bool on;
+  PF_DEVICE void start(bool enable) {
+    on = enable;
+    for (int i = 0; i < PH_N; ++i) acc[i] = 0;
+    t = clock64();
+  }
+  PF_DEVICE void lap(int ph) {
+    if (!on) return;
+    const long long n = clock64();
+    acc[ph] += n - t;
+    t = n;
+  }
+  PF_DEVICE void flush(const AttnDesc& d) {
+    if (!on || (threadIdx.x & 31) != 0) return;
+    for (int i = 0; i < PH_N; ++i)
+      atomicAdd(reinterpret_cast<unsigned long long*>(d.trace + d.trace_cap - 64 + i), (unsigned long long)acc[i]);
+  }
+};
+#else
+struct PhaseClock {
+  long long acc[PH_N];
+  static constexpr bool on = false;
+  PF_DEVICE void start(bool) {}
+  PF_DEVICE void lap(int) {}
+  PF_DEVICE void flush(const AttnDesc&) {}
+};
+#endif
+
 struct UnitInfo {
   int q_row0, q_len, q_local0, kv_off, kv_len, q_off, n_pre, n_blk, h0, nh, g, pad;
 };
@@ -283,10 +321,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const uint32_t tO = tmem_base + lane_base + AT_TO + j * DH;
     const float sl2 = d.scale * 1.4426950408889634f;
     uint32_t blk_it = 0, u_it = 0;
+    PhaseClock pc;
+    pc.start(d.trace != nullptr);
     int k = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++k) {
       const UnitInfo ui = unit(u, k);
       if (j >= ui.nh) continue;
+      if (pc.on) pc.acc[PH_UNITS] += 1;
       const int q_local = ui.q_local0 + (int)row;
       float m_used = -INFINITY, l_run = 0.f;   // m_used in scaled (log2) units
       for (int b = 0; b < ui.n_blk; ++b, ++blk_it) {
@@ -297,7 +338,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         // spending SFU work on exp(-inf)
         const int lim_max = __reduce_max_sync(0xffffffffu, lim);
         const uint32_t tS = tS0 + 64 * (blk_it & 1);
+        pc.lap(PH_MATH);
         mbar_wait(&s_full[2 * j + (blk_it & 1)], (blk_it >> 1) & 1);
+        pc.lap(PH_SWAIT);
         if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_SFULL, k, b, j);
         tc_fence_after();
         uint32_t s[2][32];
@@ -364,7 +407,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         // Every PV phase is consumed in order: PV of this head's previous block (issued right
         // after this block's S) has finished by now, so this wait is ~free; it also guards O.
         // (A unit's last PV phase is consumed in its epilogue.)
+        pc.lap(PH_MATH);
         if (b > 0) mbar_wait(&pv_done[j], (blk_it - 1) & 1);
+        pc.lap(PH_PVWAIT);
         if (rescale && b > 0) {
           tc_fence_after();
           const float alpha = exp2f(m_old - m_used);
@@ -380,15 +425,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           }
         }
         l_run += bsum;
+        pc.lap(PH_RESCALE);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_ready[j]);
+        pc.lap(PH_ARRIVE);
         if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_PARRIVE, k, b, j);
       }
       // ---- unit epilogue: O / l -> bf16 -> global
+      pc.lap(PH_MATH);
       mbar_wait(&o_done[j], u_it & 1);
       mbar_wait(&pv_done[j], (blk_it - 1) & 1);
+      pc.lap(PH_ODONE);
       if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_ODONE, k, 0, j);
       ++u_it;
       tc_fence_after();
@@ -402,6 +451,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         if (lane == 0) tma_store_wait_read<0>();   // previous unit's store has left the buffer
         __syncwarp();
       }
+      pc.lap(PH_EPI_WAIT);
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(d.out) +
                                             (size_t)(ui.q_row0 + row) * (d.H * d.dh) + (ui.h0 + j) * d.dh);
 #pragma unroll 1
@@ -410,6 +460,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         tmem_ld_32x32b_x32(tO + c2 * 64, o2[0]);
         tmem_ld_32x32b_x32(tO + c2 * 64 + 32, o2[1]);
         tmem_ld_wait();
+        pc.lap(PH_EPI_LD);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = 2 * c2 + h;
@@ -432,6 +483,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
           }
         }
       }
+      pc.lap(PH_EPI_CVT);
       if (warp_full) {
         fence_proxy_async_smem();
         __syncwarp();
@@ -444,7 +496,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
       }
       if (lane == 0 && (warp & 3) == 0) att_trace(d, EV_EPI_DONE, k, 0, j);
       tc_fence_before();
+      pc.lap(PH_EPI);
     }
+    pc.flush(d);
   }
 
   if (warp < 8 && lane == 0) tma_store_wait_all<0>();
