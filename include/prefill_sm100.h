@@ -121,7 +121,8 @@ PF_API int pf_score_capture(pf_model* model, const int32_t* ids, const int32_t* 
 /* Per-op entry points (unit parity tests). */
 /* C = A[MxK] . B[NxK]^T (RoPE heads 128 wide here; pf_gemm_bf16_ex takes rope_dh 64/128)
  * with epilogue 0 bf16, 1 bf16+RoPE, 2 SwiGLU(bf16, N/2 cols),
- * 3 fp32 C += (residual add), 4 residual pair: x = xb + C held as bf16 (hi = xb, lo = C),
+ * 3 fp32 C += (residual add), 4 residual stream x = hi + lo with hi = xb (bf16, = bf16(x)) and
+ * lo = C (uint8 b, x - hi = (b - 128) * 2^(E - 142), E = the biased fp32 exponent of hi; ldc in bytes),
  * updated in place to x + acc, and ss_out[nb * ss_ld + row] = sum over n-tile nb (256 columns)
  * of (x + acc)^2 (pf_gemm_bf16_ex). */
 PF_API int pf_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N,
@@ -139,7 +140,7 @@ typedef struct pf_gemm_args {
 } pf_gemm_args;
 PF_API int pf_gemm_bf16_ex(const pf_gemm_args* args, pf_stream_t stream);
 /* Embedding gather; every output is optional (NULL skips it): resid = float(E[ids]) (fp32),
- * hi = E[ids] and lo = 0 (the bf16 residual pair the forward keeps), ss = per-row sum of squares
+ * hi = E[ids] and lo = 0x80 bytes (zero; the bf16 hi + 8-bit lo residual the forward keeps), ss = per-row sum of squares
  * in the GEMMs' partial layout: ss[t] = sum, ss[p*T + t] = 0 for 1 <= p < ceil(d/256). */
 PF_API int pf_embed(const int32_t* ids, const void* emb, float* resid, void* hi, void* lo, float* ss, int T,
              int d, pf_stream_t stream);

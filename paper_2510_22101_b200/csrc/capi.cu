@@ -77,6 +77,29 @@ bool make_tmap_2d(CUtensorMap* out, const void* base, int elem_bytes, uint64_t r
   return true;
 }
 
+bool make_tmap_2d_u8_sw64(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                          uint32_t box_rows, uint32_t box_cols) {
+  auto enc = get_encode();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return false; }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || ld % 16 != 0) {
+    set_error("tensor map: base %p / row stride %llu B not 16-byte aligned", base, (unsigned long long)ld);
+    return false;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (u8) failed (%d): rows=%llu cols=%llu ld=%llu", (int)r,
+              (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)ld);
+    return false;
+  }
+  return true;
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -95,10 +118,10 @@ constexpr size_t kAlign = 1024;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Workspace {
-  // residual stream x = hi + lo as a bf16 pair: hi = bf16(x) is the A operand of the QKV and
-  // gate/up GEMMs (their epilogues apply the fused RMSNorm), lo = bf16(x - hi)
+  // residual stream x = hi + lo: hi = bf16(x) is the A operand of the QKV and gate/up GEMMs (their
+  // epilogues apply the fused RMSNorm), lo = byte b with x - hi = (b - 128) * 2^(E(hi) - 142)
   void* xb;          // hi
-  void* rlo;         // lo
+  void* rlo;         // lo: uint8 b, x - hi = (b - 128) * 2^(E(hi) - 142) (ptx.cuh resid_decode)
   float* ss_attn;    // per-row partial sums of squares of the residual feeding the attention block
   float* ss_mlp;     // ... feeding the MLP block ([ss_parts(d)][T], see pf_internal.h)
   float* rope_cs;    // per-row cos/sin gathered for the QKV epilogue (launch_rope_gather layout)
@@ -107,7 +130,7 @@ struct Workspace {
   void* hbuf;
   void* attn_c;      // [n_items x H*dh] bf16  last-layer compacted rows
   void* hi_c;        // [n_items x d] bf16
-  void* lo_c;        // [n_items x d] bf16
+  void* lo_c;        // [n_items x d] uint8
   // device copies of host inputs/outputs (pf_score_host)
   int32_t *ids, *pos, *segs, *work, *last_idx;
   float *logits2, *p_yes;
@@ -121,7 +144,7 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   size_t off = 0;
   auto take = [&](size_t bytes) { uint8_t* p = base + off; off = align_up(off + bytes); return p; };
   w.xb = take((size_t)T * d.d_model * 2);
-  w.rlo = take((size_t)T * d.d_model * 2);
+  w.rlo = take((size_t)T * d.d_model);
   w.ss_attn = reinterpret_cast<float*>(take((size_t)ss_parts(d.d_model) * T * 4));   // [part][T]
   w.ss_mlp = reinterpret_cast<float*>(take((size_t)ss_parts(d.d_model) * T * 4));
   w.rope_cs = reinterpret_cast<float*>(take(rope_gather_floats(T, d.d_head / 2) * 4));
@@ -130,7 +153,7 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   w.hbuf = take((size_t)T * d.d_ff_pad * 2);
   w.attn_c = take((size_t)n_items * m->attn_k * 2);
   w.hi_c = take((size_t)n_items * d.d_model * 2);
-  w.lo_c = take((size_t)n_items * d.d_model * 2);
+  w.lo_c = take((size_t)n_items * d.d_model);
   w.ids = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.pos = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.segs = reinterpret_cast<int32_t*>(take((size_t)n_seg * 16));

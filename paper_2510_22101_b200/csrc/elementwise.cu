@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ 
                                                     const __nv_bfloat16* __restrict__ emb,
                                                     float* __restrict__ resid, uint4* __restrict__ hi,
                                                     uint4* __restrict__ lo, float* __restrict__ ss, int T, int d) {
+  // lo: low byte of the residual (16 per uint4); embedding rows are bf16, so lo = 0 (byte 0x80)
   pdl_launch_dependents();
   pdl_wait();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -42,8 +43,8 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ 
       dst[2 * i] = make_float4(a.x, a.y, b.x, b.y);
       dst[2 * i + 1] = make_float4(c.x, c.y, f.x, f.y);
     }
-    if (hi) hi[(size_t)t * (d / 8) + i] = u;                       // embedding rows are bf16: lo = 0
-    if (lo) lo[(size_t)t * (d / 8) + i] = make_uint4(0u, 0u, 0u, 0u);
+    if (hi) hi[(size_t)t * (d / 8) + i] = u;
+    if (lo && (i & 1) == 0) lo[(size_t)t * (d / 16) + i / 2] = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
     acc += a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y + c.x * c.x + c.y * c.y + f.x * f.x + f.y * f.y;
   }
   if (ss) {
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 // One warp per item: never forms [N x V] logits — only the yes/no columns of W_head are read.
 __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ resid,
                                                    const __nv_bfloat16* __restrict__ rhi,
-                                                   const __nv_bfloat16* __restrict__ rlo,
+                                                   const uint8_t* __restrict__ rlo,
                                                    const int32_t* __restrict__ last_idx,
                                                    int n_items, int d,
                                                    const float* __restrict__ g,
@@ -107,8 +108,9 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ res
   const int lane = threadIdx.x & 31;
   if (i >= n_items) return;
   const size_t r = (size_t)(last_idx ? __ldg(last_idx + i) : i) * d;
-  auto X = [&](int j) -> float {   // residual value: fp32, or the bf16 hi/lo pair
-    return resid ? resid[r + j] : __bfloat162float(rhi[r + j]) + __bfloat162float(rlo[r + j]);
+  auto X = [&](int j) -> float {   // residual value: fp32, or hi (bf16) + lo (byte; resid_decode)
+    if (resid) return resid[r + j];
+    return resid_decode(__bfloat162float(rhi[r + j]), rlo[r + j], 0);
   };
   float ss = 0.f;
   for (int j = lane; j < d; j += 32) { const float v = X(j); ss += v * v; }
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ res
 
 // ---------------------------------------------------------------- last-row gather
 // Compacts the rows the head needs (one per item) before the last layer's O-projection + MLP:
-// attn_c[i] = attn[last_idx[i]] (bf16), resid_c[i] = resid[last_idx[i]] (fp32).
+// attn_c[i] = attn[last_idx[i]] (bf16), hi_c/lo_c[i] = the residual row (bf16 hi, uint8 lo).
 __global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restrict__ last_idx, int n,
                                                           const uint4* __restrict__ attn, int attn_v4,
                                                           const uint4* __restrict__ hi, const uint4* __restrict__ lo,
@@ -145,10 +147,8 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restr
   if (i >= n) return;
   const size_t r = (size_t)__ldg(last_idx + i);
   for (int j = lane; j < attn_v4; j += 32) attn_c[(size_t)i * attn_v4 + j] = __ldg(attn + r * attn_v4 + j);
-  for (int j = lane; j < resid_v4; j += 32) {
-    hi_c[(size_t)i * resid_v4 + j] = __ldg(hi + r * resid_v4 + j);
-    lo_c[(size_t)i * resid_v4 + j] = __ldg(lo + r * resid_v4 + j);
-  }
+  for (int j = lane; j < resid_v4; j += 32) hi_c[(size_t)i * resid_v4 + j] = __ldg(hi + r * resid_v4 + j);
+  for (int j = lane; j < resid_v4 / 2; j += 32) lo_c[(size_t)i * resid_v4 / 2 + j] = __ldg(lo + r * resid_v4 / 2 + j);
 }
 
 int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const void* hi,
@@ -164,12 +164,12 @@ int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int att
 
 // Calibration capture ("capture flag records MLP inputs for the pruning module"):
 // out[i, :] = rmsnorm(x[rows[i]]) * g, the MLP block's input, for the sampled packed rows.  x is the
-// residual pair hi + lo after the O-projection and ss its per-row partial sums of squares
+// residual hi (bf16) + lo (uint8 byte) after the O-projection and ss its per-row partial sums of squares
 // ([ss_parts(d)][ss_ld], summed in order; final once the preceding GEMM completes).  One warp per
 // captured row, 8 columns per lane step.
 __global__ void __launch_bounds__(256) capture_rows_kernel(const int32_t* __restrict__ rows, int n,
                                                            const uint4* __restrict__ hi,
-                                                           const uint4* __restrict__ lo,
+                                                           const uint2* __restrict__ lo,
                                                            const float* __restrict__ ss, int ss_ld,
                                                            const float* __restrict__ g, int d_v8, float inv_d,
                                                            float eps, float* __restrict__ out) {
@@ -185,16 +185,13 @@ __global__ void __launch_bounds__(256) capture_rows_kernel(const int32_t* __rest
   float4* o = reinterpret_cast<float4*>(out + (size_t)i * d_v8 * 8);
   const float4* g4 = reinterpret_cast<const float4*>(g);
   for (int j = lane; j < d_v8; j += 32) {
-    const uint4 h = __ldg(hi + r * d_v8 + j), l = __ldg(lo + r * d_v8 + j);
-    const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+    const uint4 h = __ldg(hi + r * d_v8 + j);
+    const uint2 l = __ldg(lo + r * d_v8 + j);
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[2] = {l.x, l.y};
     float x[8];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hw[e]);
-      const __nv_bfloat162 lb = *reinterpret_cast<const __nv_bfloat162*>(&lw[e]);
-      x[2 * e] = __bfloat162float(hb.x) + __bfloat162float(lb.x);
-      x[2 * e + 1] = __bfloat162float(hb.y) + __bfloat162float(lb.y);
-    }
+    for (int e = 0; e < 8; ++e)
+      x[e] = resid_decode(__uint_as_float((e & 1) ? hw[e / 2] & 0xffff0000u : hw[e / 2] << 16), lw[e / 4], e & 3);
     const float4 ga = __ldg(g4 + 2 * j), gb = __ldg(g4 + 2 * j + 1);
     o[2 * j] = make_float4(x[0] * rs * ga.x, x[1] * rs * ga.y, x[2] * rs * ga.z, x[3] * rs * ga.w);
     o[2 * j + 1] = make_float4(x[4] * rs * gb.x, x[5] * rs * gb.y, x[6] * rs * gb.z, x[7] * rs * gb.w);
@@ -236,7 +233,7 @@ int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* 
   if (n == 0) return 0;
   if (d % 8 != 0) return fail(-2, "capture: d_model must be a multiple of 8");
   capture_rows_kernel<<<(n + 7) / 8, 256, 0, stream>>>(rows, n, reinterpret_cast<const uint4*>(hi),
-                                                        reinterpret_cast<const uint4*>(lo), ss, ss_ld, g, d / 8,
+                                                        reinterpret_cast<const uint2*>(lo), ss, ss_ld, g, d / 8,
                                                         1.0f / (float)d, eps, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "capture launch: %s", cudaGetErrorString(e));
@@ -244,7 +241,7 @@ int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* 
 
 int launch_embed(const int32_t* ids, const void* emb, float* resid, void* hi, void* lo, float* ss, int T,
                  int d, cudaStream_t stream) {
-  if (d % 8 != 0) return fail(-2, "embed: d_model must be a multiple of 8");
+  if (d % 16 != 0) return fail(-2, "embed: d_model must be a multiple of 16");
   if (T == 0) return 0;
   embed_kernel<<<(T + 7) / 8, 256, 0, stream>>>(ids, reinterpret_cast<const __nv_bfloat16*>(emb), resid,
                                                 reinterpret_cast<uint4*>(hi), reinterpret_cast<uint4*>(lo), ss,
@@ -277,7 +274,7 @@ int launch_head(const float* resid, const void* rhi, const void* rlo, const int3
                 float* p_yes, int* bad, cudaStream_t stream) {
   if (n_items == 0) return 0;
   head_kernel<<<(n_items + 7) / 8, 256, 0, stream>>>(resid, reinterpret_cast<const __nv_bfloat16*>(rhi),
-                                                     reinterpret_cast<const __nv_bfloat16*>(rlo), last_idx,
+                                                     reinterpret_cast<const uint8_t*>(rlo), last_idx,
                                                      n_items, d, g, w_yes, w_no, eps, logits2, p_yes, bad);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : fail(-4, "head launch: %s", cudaGetErrorString(e));

@@ -31,12 +31,13 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 // CG = CTAs per MMA (cta_group).  CG=2: a CTA pair computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 (M=256); each CTA loads its own 128 A rows and half (128) of the
 // B rows, so per-CTA operand bytes per MMA drop from 48 KB to 32 KB per k-block.
-// EPI_RESID_ADD_NORM reads the old residual (bf16 hi/lo pair) through a per-warp ring of
-// RB_DEPTH TMA-loaded 64-column chunks (hi box + lo box, 8 KB), updating it in place; it trades
+// EPI_RESID_ADD_NORM reads the old residual (bf16 hi + 8-bit lo, 3 B/elem) through a per-warp ring of
+// RB_DEPTH TMA-loaded 64-column chunks (hi box 4 KB + lo box 2 KB), updating it in place; it trades
 // mainloop stages for that ring (PF_RING_STAGES / PF_RB_DEPTH override for A/B builds).  5 stages +
 // depth 2 beat 4 + 3 by 2-8 us at the C4 shapes (tools/epi_sweep.py, profiles/r01/epi_sweep.txt):
-// the epilogue math is free (hidden under the MMAs); its 8 B/elem of residual traffic is not, it
-// competes with the mainloop's operand loads in L2 / HBM (~+20 us per GEMM each).
+// the epilogue math is free (hidden under the MMAs); its residual traffic is not, it competes with
+// the mainloop's operand loads in L2 / HBM.  An 8-bit low word (6 B/elem read + write) instead of a
+// bf16 one (8 B/elem) took C4 from 35.5 to ~34.6 ms/step at unchanged parity margins.
 #ifndef PF_RB_DEPTH
 #define PF_RB_DEPTH 2
 #endif
@@ -44,7 +45,8 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 #define PF_RING_STAGES 5
 #endif
 constexpr int RB_DEPTH = PF_RB_DEPTH;
-constexpr int RB_SLOT = 2 * GEMM_STG_BYTES;           // hi + lo boxes of one 64-column chunk
+constexpr int RB_LO_BYTES = 32 * 64;                 // one 32-row x 64 B uint8 box (64B swizzle)
+constexpr int RB_SLOT = GEMM_STG_BYTES + RB_LO_BYTES; // hi + lo boxes of one 64-column chunk (1 KB multiple)
 template <int CG, int EPI>
 struct GemmCfg {
   static constexpr int B_ROWS = GEMM_BN / CG;                // B rows loaded per CTA
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (lane == 0) {
         mbar_arrive_expect_tx(&my_rbar[b], RB_SLOT);
         tma_load_2d(my_stg + b * RB_SLOT, &tmD, &my_rbar[b], nn, mm, kEvictFirst);                    // hi
-        tma_load_2d(my_stg + b * RB_SLOT + GEMM_STG_BYTES, &tmC, &my_rbar[b], nn, mm, kEvictFirst);   // lo
+        tma_load_2d(my_stg + b * RB_SLOT + GEMM_STG_BYTES, &tmC, &my_rbar[b], nn, mm, kEvictFirst);   // lo (uint8)
       }
       ++ring_issued;
     };
@@ -329,11 +331,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           emit(v, n0 + c * 32, r0);
         }
       } else if constexpr (EPI == EPI_RESID_ADD_NORM) {
-        // Residual stream as a bf16 pair: x = hi + lo, hi = bf16(x) (the next GEMM's A operand),
-        // lo = bf16(x - hi) (~16 mantissa bits together).  new = hi + lo + acc in fp32; hi/lo are
-        // rewritten in place in the ring slot and leave by TMA store; ss_out[nb][row] = sum(new^2)
-        // (next RMSNorm).  Old chunks arrive through the TMA ring (the first RB_DEPTH issued while
-        // this tile's MMAs ran).  Bulk groups: one per chunk (hi + lo stores).
+        // Residual stream x = hi + lo: hi = bf16(x) (the next GEMM's A operand), lo = byte b with
+        // x - hi = (b - 128) * 2^(E(hi) - 142) (resid_decode, ptx.cuh; ~16 significant bits together).
+        // new = hi + lo + acc in fp32; hi/lo are rewritten in place in the ring slot and leave by TMA
+        // store; ss_out[nb][row] = sum(new^2) (next RMSNorm).  Old chunks arrive through the TMA ring
+        // (the first RB_DEPTH issued while this tile's MMAs ran).  Bulk groups: one per chunk.
         const int n_chunks = ring_chunks(tile);
         float ssq = 0.f;
 #pragma unroll 1
@@ -352,32 +354,40 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_ld_32x32b_x32(t_row + c * 64, v0);
           tmem_ld_32x32b_x32(t_row + c * 64 + 32, v1);
           const uint32_t hrow = smem_u32(my_stg + b * RB_SLOT) + lane * 128;
-          const uint32_t lrow = hrow + GEMM_STG_BYTES;
+          const uint32_t lrow = smem_u32(my_stg + b * RB_SLOT + GEMM_STG_BYTES) + lane * 64;
           tmem_ld_wait();
+          uint32_t l[4];
+          float qn[16];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {      // 16 B chunk j = columns [8j, 8j+8) of this 64-col chunk
             const uint32_t off = (j ^ (lane & 7)) << 4;
-            uint32_t h[4], l[4];
+            // lo row: 64 B, 64B swizzle (16 B unit u of row r sits at u ^ ((r >> 1) & 3)); unit j/2
+            // holds columns [16(j/2), 16(j/2)+16)
+            const uint32_t loff = ((j >> 1) ^ ((lane >> 1) & 3)) << 4;
+            uint32_t h[4];
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(h[0]), "=r"(h[1]), "=r"(h[2]), "=r"(h[3]) : "r"(hrow + off));
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(l[0]), "=r"(l[1]), "=r"(l[2]), "=r"(l[3]) : "r"(lrow + off));
-            uint32_t nh[4], nl[4];
+            if ((j & 1) == 0)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(l[0]), "=r"(l[1]), "=r"(l[2]), "=r"(l[3]) : "r"(lrow + loff));
+            uint32_t nh[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int col = 8 * j + 2 * e;      // within the 64-col chunk
+              const int kq = (j & 1) * 8 + 2 * e; // byte within the 16-col lo unit
               const float a0 = (col < 32) ? __uint_as_float(v0[col]) : __uint_as_float(v1[col - 32]);
               const float a1 = (col + 1 < 32) ? __uint_as_float(v0[col + 1]) : __uint_as_float(v1[col + 1 - 32]);
-              const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&h[e]);
-              const __nv_bfloat162 lb = *reinterpret_cast<const __nv_bfloat162*>(&l[e]);
-              const float x0 = __bfloat162float(hb.x) + __bfloat162float(lb.x) + a0;
-              const float x1 = __bfloat162float(hb.y) + __bfloat162float(lb.y) + a1;
+              const float x0 = resid_decode(__uint_as_float(h[e] << 16), l[kq >> 2], kq & 3) + a0;
+              const float x1 = resid_decode(__uint_as_float(h[e] & 0xffff0000u), l[kq >> 2], (kq + 1) & 3) + a1;
               ssq += x0 * x0 + x1 * x1;
               const __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
-              const __nv_bfloat162 l2 = __floats2bfloat162_rn(x0 - __bfloat162float(h2.x), x1 - __bfloat162float(h2.y));
-              nh[e] = *reinterpret_cast<const uint32_t*>(&h2);
-              nl[e] = *reinterpret_cast<const uint32_t*>(&l2);
+              const uint32_t hw = *reinterpret_cast<const uint32_t*>(&h2);
+              qn[kq] = resid_lo_encode(x0, __uint_as_float(hw << 16));
+              qn[kq + 1] = resid_lo_encode(x1, __uint_as_float(hw & 0xffff0000u));
+              nh[e] = hw;
             }
             st_shared_v4(hrow + off, nh[0], nh[1], nh[2], nh[3]);
-            st_shared_v4(lrow + off, nl[0], nl[1], nl[2], nl[3]);
+            if (j & 1)
+              st_shared_v4(lrow + loff, pack_lo4(qn[0], qn[1], qn[2], qn[3]), pack_lo4(qn[4], qn[5], qn[6], qn[7]),
+                           pack_lo4(qn[8], qn[9], qn[10], qn[11]), pack_lo4(qn[12], qn[13], qn[14], qn[15]));
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -624,6 +634,8 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
   const int out_cols = d.epilogue == EPI_SWIGLU ? d.N / 2 : d.N;
   if (d.epilogue == EPI_RESID_ADD) {
     if (!make_tmap_2d(&tc, d.C, 4, d.M, out_cols, d.ldc, 32, 32, true)) return -3;
+  } else if (d.epilogue == EPI_RESID_ADD_NORM) {   // 8-bit low word of the residual, 64B swizzle
+    if (!make_tmap_2d_u8_sw64(&tc, d.C, d.M, out_cols, d.ldc, 32, 64)) return -3;
   } else {
     if (!make_tmap_2d(&tc, d.C, 2, d.M, out_cols, d.ldc, 32, 64, true)) return -3;
   }

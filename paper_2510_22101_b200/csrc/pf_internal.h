@@ -12,7 +12,7 @@ enum Epilogue : int {
   EPI_ROPE_BF16 = 1,
   EPI_SWIGLU = 2,
   EPI_RESID_ADD = 3,
-  EPI_RESID_ADD_NORM = 4,   // (hi=xb, lo=C) bf16 pair += acc in place, ss_out[nb][row] = tile sum(new^2)
+  EPI_RESID_ADD_NORM = 4,   // (hi=xb bf16, lo=C uint8) residual += acc in place, ss_out[nb][row] = tile sum(new^2)
 };
 
 // ---- programmatic dependent launch switch (PF_NO_PDL=1 disables)
@@ -27,6 +27,8 @@ int fail(int code, const char* fmt, ...);
 // box = [box_rows x box_cols], 128-byte swizzle when box_cols*elem_bytes == 128.
 bool make_tmap_2d(CUtensorMap* out, const void* base, int elem_bytes, uint64_t rows, uint64_t cols,
                   uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+bool make_tmap_2d_u8_sw64(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                          uint32_t box_rows, uint32_t box_cols);
 
 // ---- launchers (return 0 or negative error code)
 struct GemmDesc {

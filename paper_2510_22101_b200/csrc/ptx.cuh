@@ -351,4 +351,27 @@ PF_DEVICE void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, u
                : "memory");
 }
 
+// Residual stream low word (8 bits): x = hi + (b - 128) * 2^(E - 142), with E the biased exponent of
+// the bf16 hi = bf16(x) and b a byte.  |x - hi| <= ulp(hi)/2 = 2^(E - 135), so b adds 8 mantissa
+// bits below hi (step ulp(hi)/256): ~16 significant bits in 3 bytes per element.  Both directions
+// are exponent-field arithmetic plus the 1.5 * 2^23 float trick (the low mantissa byte of
+// 12582912 + v is round(v) for |v| < 2^22), no int<->float conversions.
+PF_DEVICE float resid_lo_scale(float hi) {          // 2^(E - 142); 0 for hi = 0
+  return __uint_as_float(__float_as_uint(hi) & 0x7f800000u) * 0x1p-15f;
+}
+PF_DEVICE float resid_decode(float hi, uint32_t lo4, int k) {   // hi + lo, lo = byte k of lo4
+  const float q = __uint_as_float(__byte_perm(lo4, 0x4B400000u, 0x7650u | k)) - 12583040.0f;
+  return fmaf(q, resid_lo_scale(hi), hi);
+}
+// float whose low byte is the lo byte of x against hi = bf16(x) (as a float); pack with pack_lo4
+PF_DEVICE float resid_lo_encode(float x, float hi) {
+  const float inv = __uint_as_float(0x86800000u - (__float_as_uint(hi) & 0x7f800000u));   // 2^(142 - E)
+  return fminf(fmaf(x - hi, inv, 12583040.0f), 12583167.0f);   // 1.5*2^23 + 128 + v, v <= 127
+}
+PF_DEVICE uint32_t pack_lo4(float t0, float t1, float t2, float t3) {
+  const uint32_t a = __byte_perm(__float_as_uint(t0), __float_as_uint(t1), 0x0040u);
+  const uint32_t b = __byte_perm(__float_as_uint(t2), __float_as_uint(t3), 0x0040u);
+  return __byte_perm(a, b, 0x5410u);
+}
+
 }  // namespace pf
