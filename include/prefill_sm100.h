@@ -181,6 +181,27 @@ PF_API int pf_pack_requests(const int32_t* ids, const int64_t* list_offsets, con
                             int32_t* out_segs, int32_t* out_last, int32_t* out_prefix_lens,
                             int64_t* out_T, int64_t* out_n_seg);
 
+/* In-step kernel timing (measurement only).  pf_profile_enable(1) makes every eager pf_score /
+ * pf_score_host / pf_score_capture call bracket each launch with CUDA events on its stream, tagged
+ * by kernel class (PF_PROF_*); launches recorded while the stream is capturing a graph are skipped.
+ * pf_profile_read waits for the events, writes the summed ms and launch count per class and resets.
+ * Process-global, not thread-safe: one measuring thread.  An event record between two kernels ends
+ * the programmatic-dependent-launch overlap there, so the per-class sums slightly exceed a graph
+ * replay's step time. */
+enum {
+  PF_PROF_ELEMENTWISE = 0, /* embed, rope cos/sin gather, head */
+  PF_PROF_QKV = 1,         /* QKV GEMM + RoPE epilogue */
+  PF_PROF_ATTENTION = 2,
+  PF_PROF_O_PROJ = 3,      /* O GEMM + residual + RMSNorm statistic */
+  PF_PROF_GATE_UP = 4,     /* gate/up GEMM + SwiGLU epilogue */
+  PF_PROF_DOWN = 5,        /* down GEMM + residual + RMSNorm statistic */
+  PF_PROF_LAST_LAYER = 6,  /* last layer's row gather + O/gate-up/down on the n_items last rows */
+  PF_PROF_CLASSES = 7
+};
+PF_API int pf_profile_enable(int on);
+PF_API int pf_profile_read(double* ms, int* launches, int n_classes);
+PF_API const char* pf_profile_class_name(int cls);
+
 /* Debug hook: CTA 0 of the attention kernel appends {event, role, unit, block, globaltimer}
  * records (uint64) to device_buf (NULL disables).  Used by tools/attn_trace.py. */
 PF_API int pf_debug_set_trace(void* device_buf, unsigned int capacity);

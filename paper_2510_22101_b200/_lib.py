@@ -23,7 +23,7 @@ EPI_BF16, EPI_ROPE_BF16, EPI_SWIGLU, EPI_RESID_ADD, EPI_RESID_ADD_NORM = 0, 1, 2
 EXPORTED_SYMBOLS = (
     "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host", "pf_score_capture",
     "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
-    "pf_last_error", "pf_version", "pf_debug_set_trace",
+    "pf_last_error", "pf_version", "pf_debug_set_trace", "pf_profile_enable", "pf_profile_read", "pf_profile_class_name",
     "pf_tokenize", "pf_tokenize_spans", "pf_tokenize_batch", "pf_pack_sizes", "pf_pack_requests",
 )
 
@@ -103,6 +103,9 @@ _SIGS = {
     "pf_tokenize_batch": (_I, [_P, _P, _I, _I, _I, _P, ctypes.c_int64, _P, _I]),
     "pf_pack_sizes": (_I, [_P, _P, _I, _P, _P, _P]),
     "pf_pack_requests": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "pf_profile_enable": (_I, [_I]),
+    "pf_profile_read": (_I, [_P, _P, _I]),
+    "pf_profile_class_name": (ctypes.c_char_p, [_I]),
     "pf_last_error": (ctypes.c_char_p, []),
     "pf_version": (ctypes.c_char_p, []),
 }

@@ -232,6 +232,49 @@ size_t pf_workspace_bytes(const pf_model* model, int T, int n_items) {
   return layout(model, T, n_items, T, T, nullptr).total + kAlign;
 }
 
+// ---------------------------------------------------------------- in-step kernel timing
+// pf_profile_enable(1): every eager pf_score* call brackets each launch with a pair of CUDA events on
+// its stream, tagged with the kernel class; pf_profile_read sums them per class.  Skipped while the
+// stream is being captured into a graph.  Measurement only: an event record between two kernels
+// also ends the programmatic-dependent-launch overlap at that point.
+namespace {
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // 2 per slot
+  std::vector<int> cls;
+  size_t used = 0;
+};
+Profiler g_prof;
+
+struct ProfScope {
+  cudaStream_t st;
+  long idx = -1;
+  ProfScope(int c, cudaStream_t s) : st(s) {
+    if (!g_prof.on) return;
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    if (g_prof.used == g_prof.cls.size()) {
+      cudaEvent_t a, b;
+      if (cudaEventCreate(&a) != cudaSuccess) return;
+      if (cudaEventCreate(&b) != cudaSuccess) { cudaEventDestroy(a); return; }
+      g_prof.ev.push_back(a);
+      g_prof.ev.push_back(b);
+      g_prof.cls.push_back(c);
+    }
+    idx = (long)g_prof.used++;
+    g_prof.cls[idx] = c;
+    cudaEventRecord(g_prof.ev[2 * idx], st);
+  }
+  ~ProfScope() {
+    if (idx >= 0) cudaEventRecord(g_prof.ev[2 * idx + 1], st);
+  }
+};
+const char* const kProfNames[PF_PROF_CLASSES] = {"elementwise", "qkv_rope", "attention", "o_proj",
+                                                 "gate_up",     "down",     "last_layer"};
+}  // namespace
+
+#define PF_PROF(c) ProfScope _pf_prof_scope_##__LINE__(c, st)
+
 static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
                        int n_seg, const int32_t* work, int n_work, const int32_t* last_idx,
                        int n_items, int T, const Workspace& w, float* logits2, float* p_yes,
@@ -244,10 +287,13 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
   // per-n-tile partials; the next GEMM sums them in order and scales its accumulator rows by
   // rsqrt(ss/d + eps): no atomics, so a pass is bit-reproducible (norm gains are folded into
   // w_qkv / w_gu by the caller, include/prefill_sm100.h).
-  int rc = launch_embed(ids, d.embedding, nullptr, w.xb, w.rlo, w.ss_attn, T, d.d_model, st);
-  if (rc) return rc;
-  // positions are fixed for the pass: gather each row's cos/sin once into the coalesced layout
-  if ((rc = launch_rope_gather(pos, d.rope_cos, d.rope_sin, d.d_head / 2, T, w.rope_cs, st))) return rc;
+  int rc;
+  {
+    PF_PROF(PF_PROF_ELEMENTWISE);
+    if ((rc = launch_embed(ids, d.embedding, nullptr, w.xb, w.rlo, w.ss_attn, T, d.d_model, st))) return rc;
+    // positions are fixed for the pass: gather each row's cos/sin once into the coalesced layout
+    if ((rc = launch_rope_gather(pos, d.rope_cos, d.rope_sin, d.d_head / 2, T, w.rope_cs, st))) return rc;
+  }
   for (int l = 0; l < d.n_layers; ++l) {
     GemmDesc g{};
     g.A = w.xb; g.lda = d.d_model; g.B = d.w_qkv[l]; g.ldb = d.d_model;
@@ -256,14 +302,21 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     g.rope_heads = d.n_heads + d.n_kv_heads; g.rope_dh = d.d_head; g.max_seq = d.max_seq;
     g.rope_cs = w.rope_cs;
     g.row_ss = w.ss_attn; g.ss_ld = T; g.inv_d = inv_d; g.eps = eps;
-    if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
+    {
+      PF_PROF(PF_PROF_QKV);
+      if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
+    }
     AttnDesc a{};
     a.qkv = w.qkv; a.out = w.attn; a.T = T; a.H = d.n_heads; a.Hkv = d.n_kv_heads; a.dh = d.d_head;
     a.work = work; a.n_work = n_work; a.segs = segs; a.scale = 1.0f / sqrtf((float)d.d_head);
-    if ((rc = launch_attention(a, st))) return rc;
+    {
+      PF_PROF(PF_PROF_ATTENTION);
+      if ((rc = launch_attention(a, st))) return rc;
+    }
     if (l == d.n_layers - 1 && n_items < T && m->last_layer_compact && cap == nullptr) {
       // Last layer: only the n_items last-token rows reach the head, so the O-projection and MLP
       // run on those rows alone (per-row arithmetic unchanged; tests check bit-equality).
+      PF_PROF(PF_PROF_LAST_LAYER);
       if ((rc = launch_gather_rows(last_idx, n_items, w.attn, m->attn_k, w.xb, w.rlo, d.d_model, w.attn_c,
                                    w.hi_c, w.lo_c, st)))
         return rc;
@@ -289,7 +342,10 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     o.A = w.attn; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
     o.C = w.rlo; o.ldc = d.d_model; o.M = T; o.N = d.d_model; o.K = m->attn_k;
     o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp; o.ss_ld = T;
-    if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
+    {
+      PF_PROF(PF_PROF_O_PROJ);
+      if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
+    }
     if (cap != nullptr &&
         (rc = launch_capture_rows(cap->rows, cap->n_rows, w.xb, w.rlo, w.ss_mlp, T, cap->gains + (size_t)l * d.d_model,
                                   d.d_model, eps,
@@ -301,13 +357,20 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     gu.A = w.xb; gu.lda = d.d_model; gu.B = d.w_gu[l]; gu.ldb = d.d_model;
     gu.C = w.hbuf; gu.ldc = d.d_ff_pad; gu.M = T; gu.N = 2 * d.d_ff_pad; gu.K = d.d_model;
     gu.epilogue = EPI_SWIGLU; gu.row_ss = w.ss_mlp; gu.ss_ld = T; gu.inv_d = inv_d; gu.eps = eps;
-    if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
+    {
+      PF_PROF(PF_PROF_GATE_UP);
+      if ((rc = launch_gemm(gu, &m->tm_gu[l], st))) return rc;
+    }
     GemmDesc dn{};
     dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
     dn.C = w.rlo; dn.ldc = d.d_model; dn.M = T; dn.N = d.d_model; dn.K = d.d_ff_pad;
     dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.xb; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn; dn.ss_ld = T;
-    if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
+    {
+      PF_PROF(PF_PROF_DOWN);
+      if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
+    }
   }
+  PF_PROF(PF_PROF_ELEMENTWISE);
   return launch_head(nullptr, w.xb, w.rlo, last_idx, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no, eps,
                      logits2, p_yes, bad, st);
 }
@@ -456,3 +519,28 @@ int pf_head_last_token(const float* resid, const int32_t* last_idx, int n_items,
 }
 
 }  // extern "C"
+
+int pf_profile_enable(int on) {
+  g_prof.on = on != 0;
+  g_prof.used = 0;
+  return 0;
+}
+
+int pf_profile_read(double* ms, int* launches, int n_classes) {
+  if (!ms || !launches || n_classes < 1) return fail(-1, "pf_profile_read: bad arguments");
+  for (int c = 0; c < n_classes; ++c) { ms[c] = 0.0; launches[c] = 0; }
+  for (size_t i = 0; i < g_prof.used; ++i) {
+    cudaError_t e = cudaEventSynchronize(g_prof.ev[2 * i + 1]);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]);
+    if (e != cudaSuccess) return fail(-4, "pf_profile_read: %s", cudaGetErrorString(e));
+    const int c = g_prof.cls[i];
+    if (c < n_classes) { ms[c] += t; launches[c] += 1; }
+  }
+  g_prof.used = 0;
+  return 0;
+}
+
+const char* pf_profile_class_name(int cls) {
+  return (cls >= 0 && cls < PF_PROF_CLASSES) ? kProfNames[cls] : "";
+}

@@ -223,6 +223,39 @@ def test_host_path_rejects_malformed_batches():
     scorer.score_host(PinnedPacked(good))   # still healthy afterwards
 
 
+def test_in_step_kernel_profiler():
+    """pf_profile_*: per-class event timing of eager passes (bench.py's in-step roofline); launches
+    captured into a graph are not recorded; profiling leaves the scores unchanged."""
+    import ctypes
+
+    from paper_2510_22101_b200 import _lib
+    from paper_2510_22101_b200.engine import DevicePacked
+
+    lib = _lib.load()
+    cfg, scorer, _ = get_models("TINY_GQA")
+    rng = np.random.default_rng(19)
+    packed = pack_requests([make_shared(rng, 64, list(rng.integers(1, 300, 12)), "spread")])
+    direct = scorer.score_packed(packed)
+    dp = DevicePacked(packed, scorer.device)
+    _lib.check(lib.pf_profile_enable(1))
+    run = scorer.graph_runner(dp)        # one eager warm-up pass (recorded), then the capture (not)
+    run()
+    for _ in range(2):
+        scorer.score_device(dp, check=False)
+    ms, nl = (ctypes.c_double * 7)(), (ctypes.c_int * 7)()
+    _lib.check(lib.pf_profile_read(ms, nl, 7))
+    _lib.check(lib.pf_profile_enable(0))
+    L = cfg.n_layers
+    names = [lib.pf_profile_class_name(c).decode() for c in range(7)]
+    assert names == ["elementwise", "qkv_rope", "attention", "o_proj", "gate_up", "down", "last_layer"]
+    P = 3                                # eager passes: graph_runner's warm-up + 2
+    # per pass: embed/rope-gather scope (the head runs inside the compacted last layer's scope)
+    assert list(nl) == [P, P * L, P * L, P * (L - 1), P * (L - 1), P * (L - 1), P]
+    assert all(ms[c] > 0 for c in range(7))
+    res = scorer.score_packed(packed)
+    np.testing.assert_array_equal(res.p_yes, direct.p_yes)
+
+
 def test_graph_replay_matches_direct():
     from paper_2510_22101_b200.engine import DevicePacked
 

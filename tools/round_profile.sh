@@ -12,7 +12,7 @@ for c in C4 C2; do
 done
 for k in "attn_prefix:attn" "gemm_bf16_kernel<1:qkv_rope" "gemm_bf16_kernel<2:gateup_swiglu" "gemm_bf16_kernel<4:resid_norm"; do
   pat=${k%%:*}; name=${k##*:}
-  timeout 600 ncu --set full --import-source on --clock-control none -k "regex:$pat" -s 30 -c 1 -o $out/${name}_c4 \
+  timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$pat" -s 30 -c 1 -o $out/${name}_c4 \
     python tools/profile_step.py --config C4 > /dev/null 2>&1
 done
 ls -la $out
