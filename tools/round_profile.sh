@@ -10,7 +10,7 @@ for c in C4 C2; do
     python tools/profile_step.py --config $c > /dev/null 2>&1
   python tools/launch_breakdown.py $out/launches_$c.csv > $out/launch_breakdown_$c.txt 2>&1
 done
-for k in "attn_prefix:attn" "gemm_bf16_kernel<1:qkv_rope" "gemm_bf16_kernel<2:gateup_swiglu" "gemm_bf16_kernel<4:resid_norm"; do
+for k in "attn_prefix:attn" "gemm_bf16_kernel<.int.1,:qkv_rope" "gemm_bf16_kernel<.int.2,:gateup_swiglu" "gemm_bf16_kernel<.int.4,:resid_norm"; do
   pat=${k%%:*}; name=${k##*:}
   timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$pat" -s 30 -c 1 -o $out/${name}_c4 \
     python tools/profile_step.py --config C4 > /dev/null 2>&1
