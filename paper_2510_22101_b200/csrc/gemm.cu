@@ -283,6 +283,45 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
       const int n0 = (tile % args.num_n_blk) * GEMM_BN;
       const int r0 = m0 + quad * 32;
+      const int grow = m0 + (int)row;
+      const bool rvalid = grow < args.M;
+      // Global loads that do not depend on the accumulator are issued before waiting for it, so
+      // their latency hides behind the mainloop: the fused-RMSNorm row statistics and (RoPE) the
+      // first cos/sin block of this row.
+      float rs = 1.f;
+      if (args.row_ss != nullptr && rvalid) {
+        // the A rows were bf16(residual): scale the accumulator row by rstd.  Partials summed in a
+        // fixed order: bit-reproducible (no atomics anywhere on the path)
+        float ssum = 0.f;
+#pragma unroll 8
+        for (int p = 0; p < args.ss_parts_in; ++p) ssum += __ldg(args.row_ss + (size_t)p * args.ss_ld + grow);
+        rs = rsqrtf(ssum * args.inv_d + args.eps);
+      }
+      [[maybe_unused]] float4 cv[8], sv[8];
+      [[maybe_unused]] const float4* cs4 = nullptr;
+      [[maybe_unused]] const float4* sn4 = nullptr;
+      [[maybe_unused]] int qstride = 1;
+      if constexpr (EPI == EPI_ROPE_BF16) {
+        // cos/sin of this row: gathered layout (coalesced: quad q of the warp's 32 rows is 512
+        // contiguous bytes, stride 32 float4) or the tables' row p (32 lines per warp load)
+        const int half = args.rope_dh / 2;
+        const int qn = half / 4;
+        if (args.rope_cs != nullptr) {
+          cs4 = reinterpret_cast<const float4*>(args.rope_cs) + (size_t)(r0 / 32) * 2 * qn * 32 + lane;
+          sn4 = cs4 + (size_t)qn * 32;
+          qstride = 32;
+        } else {
+          const int p = rvalid ? __ldg(args.pos + grow) : 0;
+          cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * half);
+          sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
+        }
+        const bool row_rot = r0 < args.M;   // rows past M are padding (the gathered table ends there)
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          cv[j4] = row_rot ? __ldg(cs4 + j4 * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
+          sv[j4] = row_rot ? __ldg(sn4 + j4 * qstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((quad * 32) << 16) + acc * GEMM_BN;
@@ -296,17 +335,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           else mbar_arrive_relaxed(&tempty_bar[acc]);
         }
       };
-      const int grow = m0 + (int)row;
-      const bool rvalid = grow < args.M;
-      // fused RMSNorm: the A rows were bf16(residual); scale the accumulator row by rstd
-      float rs = 1.f;
-      if (args.row_ss != nullptr && rvalid) {
-        // partials summed in a fixed order: bit-reproducible (no atomics anywhere on the path)
-        float ssum = 0.f;
-#pragma unroll 4
-        for (int p = 0; p < args.ss_parts_in; ++p) ssum += __ldg(args.row_ss + (size_t)p * args.ss_ld + grow);
-        rs = rsqrtf(ssum * args.inv_d + args.eps);
-      }
 
       if constexpr (EPI == EPI_BF16) {
 #pragma unroll 1
@@ -449,33 +477,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int cpb = half / 32;                    // 32-col blocks per head half (1 or 2)
         const int hpt = GEMM_BN / dh;                 // heads per tile (2 or 4)
         const int n_items = cpb * hpt;                // 4 for both head widths
-        const int p = rvalid ? __ldg(args.pos + grow) : 0;
-        // cos/sin of this row: gathered layout (coalesced: quad q of the warp's 32 rows is 512
-        // contiguous bytes, stride 32 float4) or the tables' row p (32 lines per warp load)
-        const int qn = half / 4;
-        const bool gathered = args.rope_cs != nullptr;
-        const float4* cs4;
-        const float4* sn4;
-        int qstride;
-        if (gathered) {
-          cs4 = reinterpret_cast<const float4*>(args.rope_cs) + (size_t)(r0 / 32) * 2 * qn * 32 + lane;
-          sn4 = cs4 + (size_t)qn * 32;
-          qstride = 32;
-        } else {
-          cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * half);
-          sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
-          qstride = 1;
-        }
         const bool row_rot = r0 < args.M;   // rows past M are padding (the gathered table ends there)
         const uint32_t stg0 = smem_u32(my_stg);
         uint32_t x1[32], x2[32];
         tmem_ld_32x32b_x32(t_row, x1);
         tmem_ld_32x32b_x32(t_row + half, x2);
-        float4 cv[8], sv[8];
 #pragma unroll 1
         for (int it = 0; it < n_items; ++it) {
           const int c = it / hpt, hd = it % hpt;
-          if (hd == 0) {
+          if (hd == 0 && c > 0) {   // block 0 was loaded before the accumulator wait
 #pragma unroll
             for (int j4 = 0; j4 < 8; ++j4) {
               cv[j4] = row_rot ? __ldg(cs4 + (c * 8 + j4) * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
