@@ -167,6 +167,13 @@ def run_reference(args):
     ws, rank, _ = dist_info()
     if rank != 0:
         return
+    # torchrun sets OMP_NUM_THREADS=1 per rank; the reference arm runs on rank 0 alone and may use
+    # every host core for its BLAS calls
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count(), user_api="blas")
+    except Exception:
+        pass
     from paper_2510_22101_b200 import CONFIGS, REQUESTS
 
     cfg, shape = CONFIGS[args.config], REQUESTS[args.config]
@@ -211,8 +218,16 @@ def run_ours(args):
     from paper_2510_22101_b200.engine import DevicePacked, PinnedPacked, PrefillScorer
 
     ws, rank, local = dist_info()
+    # PF_BENCH_SAME_DEVICE=1 (+ PF_BENCH_DIST_BACKEND=gloo): every rank on cuda:0, to exercise the
+    # multi-rank path on a one-GPU box (NCCL refuses two ranks on one device).  Not for measurements.
+    if os.environ.get("PF_BENCH_SAME_DEVICE") == "1":
+        local = 0
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PF_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg, shape = CONFIGS[args.config], REQUESTS[args.config]
@@ -239,7 +254,8 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if ws == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=dev if dist.get_backend() == "nccl" else torch.device("cpu"))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -251,7 +267,8 @@ def run_ours(args):
     if int(scorer._bad[0].item()) != 0:
         raise RuntimeError("non-finite logits in warm-up")
 
-    clocks = ClockSampler([local] if ws == 1 else list(range(ws))) if rank == 0 else None
+    n_vis = torch.cuda.device_count()
+    clocks = ClockSampler([local] if ws == 1 else list(range(min(ws, n_vis)))) if rank == 0 else None
     # ---------------------------------------------------------------- device-resident timing
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
