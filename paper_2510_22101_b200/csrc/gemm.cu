@@ -24,7 +24,7 @@ namespace pf {
 constexpr int GEMM_BM = 128;                          // rows per CTA (TMEM lanes)
 constexpr int GEMM_BN = 256;                          // output columns per tile (both CG modes)
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 192;
+
 constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
 constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B staging box
 
@@ -44,6 +44,11 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 #ifndef PF_RING_STAGES
 #define PF_RING_STAGES 5
 #endif
+// Epilogue warps of the RoPE (QKV) GEMM: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
+// taking one 128-column half of the tile).
+#ifndef PF_ROPE_EPI_WARPS
+#define PF_ROPE_EPI_WARPS 4
+#endif
 constexpr int RB_DEPTH = PF_RB_DEPTH;
 constexpr int RB_LO_BYTES = 32 * 64;                 // one 32-row x 64 B uint8 box (64B swizzle)
 constexpr int RB_SLOT = GEMM_STG_BYTES + RB_LO_BYTES; // hi + lo boxes of one 64-column chunk (1 KB multiple)
@@ -60,6 +65,8 @@ struct GemmCfg {
   static constexpr int EPI_BYTES = RING ? 4 * RB_DEPTH * RB_SLOT : 4 * (ROPE ? 4 : 2) * GEMM_STG_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
   static constexpr int TILE_M = GEMM_BM * CG;
+  static constexpr int EPI_WARPS = ROPE ? PF_ROPE_EPI_WARPS : 4;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
 };
 
 struct GemmArgs {
@@ -103,7 +110,7 @@ PF_DEVICE void stage_row_128B(uint32_t stg, uint32_t row, const uint32_t (&w)[32
 }
 
 template <int EPI, int CG>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
                      const GemmArgs args) {
@@ -141,7 +148,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4 * CG);   // every epilogue warp of the group arrives
+      mbar_init(&tempty_bar[a], Cfg::EPI_WARPS * CG);   // every epilogue warp of the group arrives
     }
     if constexpr (Cfg::RING)
       for (int i = 0; i < 4 * RB_DEPTH; ++i) mbar_init(&rbar[i], 1);
@@ -228,10 +235,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else {
-    // -------------------------------------------------------------- epilogue (warps 2..5)
+    // -------------------------------------------------------------- epilogue (warps 2..)
     const uint32_t quad = warp & 3;          // TMEM lane quadrant this warp may access
     const uint32_t row = quad * 32 + lane;   // row within the 128-row tile
-    uint8_t* my_stg = sStg + (warp - 2) * (Cfg::EPI_BYTES / 4);
+    uint8_t* my_stg = sStg + (warp - 2) * (Cfg::EPI_BYTES / Cfg::EPI_WARPS);
     int stg_idx = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -472,20 +479,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // software-pipelined (item i+1's tcgen05.ld in flight during item i's math); the whole
         // 256-column tile is staged in 4 SW128 boxes per warp and leaves by TMA after the last item,
         // so the only staging wait is for the previous tile's stores (issued a mainloop earlier).
+        // With 8 epilogue warps, warp (2 + 4 h + q) takes the heads of column half h of the tile.
+        constexpr int NH = Cfg::EPI_WARPS / 4;        // column halves: 1 or 2
         const int dh = args.rope_dh;
         const int half = dh / 2;
         const int cpb = half / 32;                    // 32-col blocks per head half (1 or 2)
         const int hpt = GEMM_BN / dh;                 // heads per tile (2 or 4)
-        const int n_items = cpb * hpt;                // 4 for both head widths
+        const int hpw = hpt / NH;                     // heads per warp
+        const int hd0 = ((int)warp - 2) / 4 * hpw;    // first head of this warp
+        const int box0 = hd0 * dh / 64;               // first 64-column staging box of this warp
+        const int n_items = cpb * hpw;
         const bool row_rot = r0 < args.M;   // rows past M are padding (the gathered table ends there)
         const uint32_t stg0 = smem_u32(my_stg);
         uint32_t x1[32], x2[32];
-        tmem_ld_32x32b_x32(t_row, x1);
-        tmem_ld_32x32b_x32(t_row + half, x2);
+        tmem_ld_32x32b_x32(t_row + hd0 * dh, x1);
+        tmem_ld_32x32b_x32(t_row + hd0 * dh + half, x2);
 #pragma unroll 1
         for (int it = 0; it < n_items; ++it) {
-          const int c = it / hpt, hd = it % hpt;
-          if (hd == 0 && c > 0) {   // block 0 was loaded before the accumulator wait
+          const int c = it / hpw, hd = hd0 + it % hpw;
+          if (hd == hd0 && c > 0) {   // block 0 was loaded before the accumulator wait
 #pragma unroll
             for (int j4 = 0; j4 < 8; ++j4) {
               cv[j4] = row_rot ? __ldg(cs4 + (c * 8 + j4) * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
@@ -514,7 +526,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             w2[j4 * 2 + 1] = pack_bf16x2(o2[2], o2[3]);
           }
           if (it + 1 < n_items) {
-            const int cn = (it + 1) / hpt, hn = (it + 1) % hpt;
+            const int cn = (it + 1) / hpw, hn = hd0 + (it + 1) % hpw;
             tmem_ld_32x32b_x32(t_row + hn * dh + cn * 32, x1);
             tmem_ld_32x32b_x32(t_row + hn * dh + half + cn * 32, x2);
           }
@@ -523,8 +535,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             __syncwarp();
           }
           const int e1 = hd * dh + c * 32, e2 = hd * dh + half + c * 32;   // tile column of each part
-          const uint32_t b1 = stg0 + (e1 / 64) * GEMM_STG_BYTES + lane * 128;
-          const uint32_t b2 = stg0 + (e2 / 64) * GEMM_STG_BYTES + lane * 128;
+          const uint32_t b1 = stg0 + (e1 / 64 - box0) * GEMM_STG_BYTES + lane * 128;
+          const uint32_t b2 = stg0 + (e2 / 64 - box0) * GEMM_STG_BYTES + lane * 128;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             const uint32_t k1 = (e1 % 64) / 8 + q4, k2 = (e2 % 64) / 8 + q4;
@@ -535,8 +547,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          for (int x = 0; x < GEMM_BN / 64; ++x)
-            if (n0 + 64 * x < args.N) tma_store_2d(&tmC, my_stg + x * GEMM_STG_BYTES, n0 + 64 * x, r0);
+          for (int x = 0; x < GEMM_BN / 64 / NH; ++x)
+            if (n0 + 64 * (box0 + x) < args.N)
+              tma_store_2d(&tmC, my_stg + x * GEMM_STG_BYTES, n0 + 64 * (box0 + x), r0);
           tma_store_commit();
         }
       }
@@ -587,7 +600,7 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
   const int grid = (tiles < groups ? tiles : groups) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
