@@ -275,6 +275,15 @@ const char* const kProfNames[PF_PROF_CLASSES] = {"elementwise", "qkv_rope", "att
 
 #define PF_PROF(c) ProfScope _pf_prof_scope_##__LINE__(c, st)
 
+static int mrev_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_GEMM_MREV");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
                        int n_seg, const int32_t* work, int n_work, const int32_t* last_idx,
                        int n_items, int T, const Workspace& w, float* logits2, float* p_yes,
@@ -342,6 +351,10 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     o.A = w.attn; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
     o.C = w.rlo; o.ldc = d.d_model; o.M = T; o.N = d.d_model; o.K = m->attn_k;
     o.epilogue = EPI_RESID_ADD_NORM; o.xb = w.xb; o.ldxb = d.d_model; o.ss_out = w.ss_mlp; o.ss_ld = T;
+    // M-order per GEMM (QKV ascending, attention last segments first, O descending, gate/up ascending,
+    // down descending): gate/up starts on the residual rows O wrote last, down on the h rows gate/up
+    // wrote last, the next QKV on the rows down wrote last
+    o.m_rev = mrev_enabled();
     {
       PF_PROF(PF_PROF_O_PROJ);
       if ((rc = launch_gemm(o, &m->tm_o[l], st))) return rc;
@@ -365,6 +378,7 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     dn.A = w.hbuf; dn.lda = d.d_ff_pad; dn.B = d.w_down[l]; dn.ldb = d.d_ff_pad;
     dn.C = w.rlo; dn.ldc = d.d_model; dn.M = T; dn.N = d.d_model; dn.K = d.d_ff_pad;
     dn.epilogue = EPI_RESID_ADD_NORM; dn.xb = w.xb; dn.ldxb = d.d_model; dn.ss_out = w.ss_attn; dn.ss_ld = T;
+    dn.m_rev = mrev_enabled();
     {
       PF_PROF(PF_PROF_DOWN);
       if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;

@@ -87,7 +87,15 @@ struct GemmArgs {
   void* xb_out;            // EPI_RESID_ADD_NORM: bf16 copy of the new residual
   int ldxb;
   float inv_d, eps;
+  int m_rev;               // walk the M blocks last-to-first (see GemmDesc::m_rev)
 };
+
+// M block of tile t: tiles run n-fastest; m_rev reverses the M order so that a consumer GEMM starts
+// on the rows its producer wrote last (still in L2)
+PF_DEVICE int m_block(const GemmArgs& a, int t) {
+  const int mb = t / a.num_n_blk;
+  return a.m_rev ? a.num_m_blk - 1 - mb : mb;
+}
 
 PF_DEVICE float4 ldg_cg_f4(const float* p) {
   float4 v;
@@ -170,7 +178,7 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = grp; tile < num_tiles; tile += ngrp) {
-      const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
+      const int m0 = m_block(args, tile) * Cfg::TILE_M + rank * GEMM_BM;
       const int n0 = (tile % args.num_n_blk) * GEMM_BN + rank * Cfg::B_ROWS;
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -267,7 +275,7 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
     uint64_t* my_rbar = rbar + (warp - 2) * RB_DEPTH;
     uint32_t ring_issued = 0, ring_used = 0;
     auto ring_issue = [&](int t, int c) {   // TMA-load chunk c (64 cols, hi + lo) of tile t's 32 rows
-      const int mm = (t / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM + quad * 32;
+      const int mm = m_block(args, t) * Cfg::TILE_M + rank * GEMM_BM + quad * 32;
       const int nn = (t % args.num_n_blk) * GEMM_BN + c * 64;
       const uint32_t b = ring_issued % RB_DEPTH;
       if (lane == 0) {
@@ -287,7 +295,7 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
       if (grp < num_tiles) ring_start(grp);
     }
     for (int tile = grp; tile < num_tiles; tile += ngrp) {
-      const int m0 = (tile / args.num_n_blk) * Cfg::TILE_M + rank * GEMM_BM;
+      const int m0 = m_block(args, tile) * Cfg::TILE_M + rank * GEMM_BM;
       const int n0 = (tile % args.num_n_blk) * GEMM_BN;
       const int r0 = m0 + quad * 32;
       const int grow = m0 + (int)row;
@@ -680,6 +688,7 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
   a.resid = reinterpret_cast<const float*>(d.C); a.ldr = d.ldc;
   a.xb_out = d.xb; a.ldxb = d.ldxb;
   a.inv_d = d.inv_d; a.eps = d.eps;
+  a.m_rev = d.m_rev;
   return cg == 2 ? dispatch_gemm<2>(d, ta, tb, tc, td, a, stream)
                  : dispatch_gemm<1>(d, ta, tb, tc, td, a, stream);
 }

@@ -49,6 +49,9 @@ struct GemmDesc {
   int rope_heads;
   int rope_dh;     // head width for the RoPE epilogue (64 or 128; 0 -> 128)
   int max_seq;
+  // 1: process M blocks last-to-first.  The forward alternates directions along producer/consumer
+  // pairs so each GEMM first reads the rows its producer wrote last (L2-resident).
+  int m_rev;
   // fused RMSNorm (see gemm.cu): A rows are bf16(residual); the epilogue multiplies row r by
   // rsqrt(sum_p row_ss[p*ss_ld + r] / d + eps) over the ceil(K/256) partial sums the producing
   // epilogue stored (fixed order: deterministic).  EPI_RESID_ADD_NORM stores its n-tile nb's
