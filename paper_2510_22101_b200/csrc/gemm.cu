@@ -171,10 +171,32 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
-  pdl_wait();   // activations / residual / row statistics come from the previous kernel
+  // activations / residual / row statistics come from the previous kernel (the producer waits below,
+  // after requesting the weights, which do not)
+  if (warp != 0) pdl_wait();
 
   if (warp == 0) {
     // -------------------------------------------------------------- TMA producer (each CTA)
+    // The first tile's first B (weight) boxes are requested before griddepcontrol.wait, so they
+    // arrive while the previous kernel drains; their stages are armed for the full A + B bytes.
+    const int pre = grp < num_tiles ? min(Cfg::STAGES, num_kb) : 0;
+    if (pre > 0) {
+      const int n0 = (grp % args.num_n_blk) * GEMM_BN + rank * Cfg::B_ROWS;
+      if (elect_one()) {
+        for (int kb = 0; kb < pre; ++kb) {
+          if constexpr (CG == 2) {
+            const uint32_t lbar = mapa_shared(smem_u32(&full_bar[kb]), 0);
+            if (leader) mbar_arrive_expect_tx(&full_bar[kb], CG * Cfg::STAGE_BYTES);
+            tma_load_2d_pair(sB + kb * Cfg::B_BYTES, &tmB, lbar, kb * GEMM_BK, n0, kEvictLast);
+          } else {
+            mbar_arrive_expect_tx(&full_bar[kb], Cfg::STAGE_BYTES);
+            tma_load_2d(sB + kb * Cfg::B_BYTES, &tmB, &full_bar[kb], kb * GEMM_BK, n0, kEvictLast);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    pdl_wait();
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = grp; tile < num_tiles; tile += ngrp) {
@@ -182,7 +204,15 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
       const int n0 = (tile % args.num_n_blk) * GEMM_BN + rank * Cfg::B_ROWS;
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
-        if (elect_one()) {
+        if (tile == grp && kb < pre) {   // B already requested, barrier armed: A only
+          if (elect_one()) {
+            if constexpr (CG == 2)
+              tma_load_2d_pair(sA + stage * GEMM_A_BYTES, &tmA, mapa_shared(smem_u32(&full_bar[stage]), 0),
+                               kb * GEMM_BK, m0, kEvictNormal);
+            else
+              tma_load_2d(sA + stage * GEMM_A_BYTES, &tmA, &full_bar[stage], kb * GEMM_BK, m0);
+          }
+        } else if (elect_one()) {
           if constexpr (CG == 2) {
             // both CTAs' bytes complete on the leader's barrier; only the leader arms it
             const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
