@@ -32,7 +32,7 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 // tcgen05.mma.cta_group::2 (M=256); each CTA loads its own 128 A rows and half (128) of the
 // B rows, so per-CTA operand bytes per MMA drop from 48 KB to 32 KB per k-block.
 // EPI_RESID_ADD_NORM reads the old residual (bf16 hi + 8-bit lo, 3 B/elem) through a per-warp ring of
-// RB_DEPTH TMA-loaded 64-column chunks (hi box 4 KB + lo box 2 KB), updating it in place; it trades
+// RBD TMA-loaded 64-column chunks (hi box 4 KB + lo box 2 KB), updating it in place; it trades
 // mainloop stages for that ring (PF_RING_STAGES / PF_RB_DEPTH override for A/B builds).  5 stages +
 // depth 2 beat 4 + 3 by 2-8 us at the C4 shapes (tools/epi_sweep.py, profiles/r01/epi_sweep.txt):
 // the epilogue math is free (hidden under the MMAs); its residual traffic is not, it competes with
@@ -49,7 +49,13 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 #ifndef PF_ROPE_EPI_WARPS
 #define PF_ROPE_EPI_WARPS 4
 #endif
-constexpr int RB_DEPTH = PF_RB_DEPTH;
+// Internal variant of EPI_RESID_ADD_NORM for short K (the C4 O projection, K = 1280): 4 mainloop stages
+// and a 4-deep ring, so a tile's whole residual (4 chunks) is requested while its MMAs run.  At K >= 2048
+// the fifth mainloop stage is worth more (tools/gemm_bench.py: C4 O 127.5 -> 123.4 us, C2 O 113 -> 116).
+constexpr int EPI_RESID_ADD_NORM_DEEP = 100;
+#ifndef PF_DEEP_RING_MAX_K
+#define PF_DEEP_RING_MAX_K 1536
+#endif
 constexpr int RB_LO_BYTES = 32 * 64;                 // one 32-row x 64 B uint8 box (64B swizzle)
 constexpr int RB_SLOT = GEMM_STG_BYTES + RB_LO_BYTES; // hi + lo boxes of one 64-column chunk (1 KB multiple)
 template <int CG, int EPI>
@@ -57,12 +63,14 @@ struct GemmCfg {
   static constexpr int B_ROWS = GEMM_BN / CG;                // B rows loaded per CTA
   static constexpr int B_BYTES = B_ROWS * GEMM_BK * 2;
   static constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
-  static constexpr bool RING = EPI == EPI_RESID_ADD_NORM;
+  static constexpr bool DEEP = EPI == EPI_RESID_ADD_NORM_DEEP;
+  static constexpr bool RING = EPI == EPI_RESID_ADD_NORM || DEEP;
+  static constexpr int RBD = DEEP ? 4 : PF_RB_DEPTH;         // ring depth (chunks in flight per warp)
   static constexpr bool ROPE = EPI == EPI_ROPE_BF16;
   // the RoPE epilogue stages a whole 256-column tile (4 boxes per warp) and gives up a stage for it
-  static constexpr int STAGES = RING ? PF_RING_STAGES : ROPE ? (CG == 2 ? 5 : 3) : (CG == 2 ? 6 : 4);
-  // ring: RB_DEPTH (hi, lo) chunk slots per epilogue warp; otherwise 2 (RoPE: 4) staging boxes per warp
-  static constexpr int EPI_BYTES = RING ? 4 * RB_DEPTH * RB_SLOT : 4 * (ROPE ? 4 : 2) * GEMM_STG_BYTES;
+  static constexpr int STAGES = DEEP ? 4 : RING ? PF_RING_STAGES : ROPE ? (CG == 2 ? 5 : 3) : (CG == 2 ? 6 : 4);
+  // ring: RBD (hi, lo) chunk slots per epilogue warp; otherwise 2 (RoPE: 4) staging boxes per warp
+  static constexpr int EPI_BYTES = RING ? 4 * RBD * RB_SLOT : 4 * (ROPE ? 4 : 2) * GEMM_STG_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
   static constexpr int TILE_M = GEMM_BM * CG;
   static constexpr int EPI_WARPS = ROPE ? PF_ROPE_EPI_WARPS : 4;
@@ -133,8 +141,8 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
   uint64_t* empty_bar = bars + Cfg::STAGES;
   uint64_t* tfull_bar = bars + 2 * Cfg::STAGES;
   uint64_t* tempty_bar = bars + 2 * Cfg::STAGES + 2;
-  uint64_t* rbar = bars + 2 * Cfg::STAGES + 4;            // [4 warps][RB_DEPTH] (ring epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4 + 4 * RB_DEPTH);
+  uint64_t* rbar = bars + 2 * Cfg::STAGES + 4;            // [4 warps][RBD] (ring epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4 + 4 * Cfg::RBD);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
       mbar_init(&tempty_bar[a], Cfg::EPI_WARPS * CG);   // every epilogue warp of the group arrives
     }
     if constexpr (Cfg::RING)
-      for (int i = 0; i < 4 * RB_DEPTH; ++i) mbar_init(&rbar[i], 1);
+      for (int i = 0; i < 4 * Cfg::RBD; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -301,13 +309,13 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
       emit_to(w, c0, r0, &tmC, EPI == EPI_RESID_ADD);
     };
 
-    // ---- EPI_RESID_ADD_NORM residual ring: chunk k of this warp lives in buffer k % RB_DEPTH
-    uint64_t* my_rbar = rbar + (warp - 2) * RB_DEPTH;
+    // ---- EPI_RESID_ADD_NORM residual ring: chunk k of this warp lives in buffer k % RBD
+    uint64_t* my_rbar = rbar + (warp - 2) * Cfg::RBD;
     uint32_t ring_issued = 0, ring_used = 0;
     auto ring_issue = [&](int t, int c) {   // TMA-load chunk c (64 cols, hi + lo) of tile t's 32 rows
       const int mm = m_block(args, t) * Cfg::TILE_M + rank * GEMM_BM + quad * 32;
       const int nn = (t % args.num_n_blk) * GEMM_BN + c * 64;
-      const uint32_t b = ring_issued % RB_DEPTH;
+      const uint32_t b = ring_issued % Cfg::RBD;
       if (lane == 0) {
         mbar_arrive_expect_tx(&my_rbar[b], RB_SLOT);
         tma_load_2d(my_stg + b * RB_SLOT, &tmD, &my_rbar[b], nn, mm, kEvictFirst);                    // hi
@@ -316,10 +324,10 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
       ++ring_issued;
     };
     auto ring_chunks = [&](int t) { return min(GEMM_BN / 64, (args.N - (t % args.num_n_blk) * GEMM_BN) / 64); };
-    // tile t's first RB_DEPTH chunks go straight into the ring (issued while its MMAs run).  An
+    // tile t's first RBD chunks go straight into the ring (issued while its MMAs run).  An
     // extra L2 prefetch of the remaining chunks was measured to make no difference.
     auto ring_start = [&](int t) {
-      for (int c = 0; c < min(RB_DEPTH, ring_chunks(t)); ++c) ring_issue(t, c);
+      for (int c = 0; c < min(Cfg::RBD, ring_chunks(t)); ++c) ring_issue(t, c);
     };
     if constexpr (Cfg::RING) {
       if (grp < num_tiles) ring_start(grp);
@@ -403,25 +411,25 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
           tmem_ld_wait();
           emit(v, n0 + c * 32, r0);
         }
-      } else if constexpr (EPI == EPI_RESID_ADD_NORM) {
+      } else if constexpr (Cfg::RING) {
         // Residual stream x = hi + lo: hi = bf16(x) (the next GEMM's A operand), lo = byte b with
         // x - hi = (b - 128) * 2^(E(hi) - 142) (resid_decode, ptx.cuh; ~16 significant bits together).
         // new = hi + lo + acc in fp32; hi/lo are rewritten in place in the ring slot and leave by TMA
         // store; ss_out[nb][row] = sum(new^2) (next RMSNorm).  Old chunks arrive through the TMA ring
-        // (the first RB_DEPTH issued while this tile's MMAs ran).  Bulk groups: one per chunk.
+        // (the first RBD issued while this tile's MMAs ran).  Bulk groups: one per chunk.
         const int n_chunks = ring_chunks(tile);
         float ssq = 0.f;
 #pragma unroll 1
         for (int c = 0; c < n_chunks; ++c) {
           const uint32_t k = ring_used;
-          const uint32_t b = k % RB_DEPTH;
-          // G(k-2) has exactly one later group: once read, its slot takes chunk c + RB_DEPTH - 2
+          const uint32_t b = k % Cfg::RBD;
+          // G(k-2) has exactly one later group: once read, its slot takes chunk c + RBD - 2
           if (c >= 2) {
             if (lane == 0) tma_store_wait_read<1>();
             __syncwarp();
-            if (c + RB_DEPTH - 2 < n_chunks) ring_issue(tile, c + RB_DEPTH - 2);
+            if (c + Cfg::RBD - 2 < n_chunks) ring_issue(tile, c + Cfg::RBD - 2);
           }
-          mbar_wait(&my_rbar[b], (k / RB_DEPTH) & 1);
+          mbar_wait(&my_rbar[b], (k / Cfg::RBD) & 1);
           ++ring_used;
           uint32_t v0[32], v1[32];
           tmem_ld_32x32b_x32(t_row + c * 64, v0);
@@ -665,7 +673,10 @@ static int dispatch_gemm(const GemmDesc& d, const CUtensorMap& ta, const CUtenso
     case EPI_ROPE_BF16: return launch_gemm_t<EPI_ROPE_BF16, CG>(ta, tb, tc, td, a, stream);
     case EPI_SWIGLU: return launch_gemm_t<EPI_SWIGLU, CG>(ta, tb, tc, td, a, stream);
     case EPI_RESID_ADD: return launch_gemm_t<EPI_RESID_ADD, CG>(ta, tb, tc, td, a, stream);
-    case EPI_RESID_ADD_NORM: return launch_gemm_t<EPI_RESID_ADD_NORM, CG>(ta, tb, tc, td, a, stream);
+    case EPI_RESID_ADD_NORM:
+      if (CG == 2 && d.K <= PF_DEEP_RING_MAX_K)
+        return launch_gemm_t<EPI_RESID_ADD_NORM_DEEP, CG>(ta, tb, tc, td, a, stream);
+      return launch_gemm_t<EPI_RESID_ADD_NORM, CG>(ta, tb, tc, td, a, stream);
     default: return fail(-2, "gemm: unknown epilogue %d", d.epilogue);
   }
 }
