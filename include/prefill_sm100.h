@@ -97,6 +97,17 @@ PF_API int pf_score_host(pf_model* model, const int32_t* ids, const int32_t* pos
                   int n_items, int T, void* workspace, size_t ws_bytes, float* logits2_host,
                   float* p_yes_host, pf_stream_t stream);
 
+/* Device-side bounds check of a packed batch already resident on the device (the pf_score inputs).
+ * Asynchronous on `stream`: err (device int[2]) receives {code, index} of a violation, {0, 0} when
+ * the batch is valid; code 1 token id outside [0, vocab), 2 position outside [0, max_seq), 3 segment
+ * outside [0, T), 4 work tile naming a missing segment or tile, 5 last_idx outside [0, T).
+ * pf_score / pf_score_capture run the same check (and wait for it, failing with -1 before any
+ * forward work) when the environment sets PF_VALIDATE=1.  No reference counterpart: the spec's
+ * shape-discipline diagnostics for a device-resident batch. */
+PF_API int pf_validate_packed(const pf_model* model, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+                              int n_seg, const int32_t* work, int n_work, const int32_t* last_idx, int n_items,
+                              int T, int* err, pf_stream_t stream);
+
 /* Calibration capture: the reference forward_prefill's `capture` flag
  * records each layer's MLP input for the pruning module.
  * pf_score_capture runs pf_score and, for every layer l, writes

@@ -19,14 +19,15 @@ __all__ = [
     "SharedBatch", "concat_packed", "merge_attention", "pack_requests", "pack_token_lists", "split_shared_prefix",
     "throughput_gain", "RankedList", "RelevanceScore", "rank_items", "relevance_score", "top_k",
     "DeviceWeights", "Weights", "init_device_weights", "init_weights", "to_device",
-    "PrefillScorer", "score_shared_batch",
+    "PrefillScorer", "score_shared_batch", "forward_prefill", "forward_with_prefix", "KVCache", "scorer_for",
     "CalibrationSet", "capture_calibration", "prune_mlp_neurons_calibrated", "sample_positions",
 ]
 
 
 def __getattr__(name):
     # engine imports torch lazily; keep `import paper_2510_22101_b200` light for CPU tooling
-    if name in ("PrefillScorer", "score_shared_batch", "ScoredBatch", "DevicePacked", "PinnedPacked"):
+    if name in ("PrefillScorer", "score_shared_batch", "ScoredBatch", "DevicePacked", "PinnedPacked",
+                "forward_prefill", "forward_with_prefix", "KVCache", "scorer_for"):
         from . import engine
         return getattr(engine, name)
     raise AttributeError(name)

@@ -99,7 +99,8 @@ def _iter_tensors(path: str):
 
 
 def load_checkpoint(path: str) -> Weights:
-    cfg, _, _ = read_header(path)
+    cfg, header, _ = read_header(path)
+    _check_header(path, cfg, header)
     ts = dict(_iter_tensors(path))
     layers = []
     for l in range(cfg.n_layers):
@@ -132,12 +133,39 @@ def model_version(path: str) -> str:
     return h.hexdigest()
 
 
+def expected_tensors(cfg: ModelConfig) -> list[tuple[str, tuple[int, ...]]]:
+    """Names and shapes of a PRLK file's tensors, in declaration order, as functions of the config
+    (SPEC.md:222 shape discipline)."""
+    from .weights import layer_shapes
+
+    shapes = {**layer_shapes(cfg), "rms_attn": (cfg.d_model,), "rms_mlp": (cfg.d_model,)}
+    out = [("token_embedding", (cfg.vocab_size, cfg.d_model))]
+    for l in range(cfg.n_layers):
+        out += [(f"layers.{l}.{n}", shapes[n]) for n in LAYER_ORDER]
+    out += [("final_norm", (cfg.d_model,)), ("head", (cfg.d_model, cfg.vocab_size))]
+    return out
+
+
+def _check_header(path: str, cfg: ModelConfig, header: dict) -> None:
+    got = [(str(n), tuple(int(x) for x in shp)) for n, shp in header.get("tensors", [])]
+    want = expected_tensors(cfg)
+    if got != want:
+        bad = next((i for i, (a, b) in enumerate(zip(got, want)) if a != b), min(len(got), len(want)))
+        g = got[bad] if bad < len(got) else "<missing>"
+        w = want[bad] if bad < len(want) else "<none>"
+        raise ValueError(f"{path}: tensor {bad} is {g}, the config requires {w} "
+                         f"({len(got)} tensors listed, {len(want)} expected)")
+
+
 def load_checkpoint_to_device(path: str, device="cuda"):
-    """PRLK -> DeviceWeights, one layer at a time (the device layout of weights.to_device)."""
+    """PRLK -> DeviceWeights, one layer at a time (the device layout of weights.to_device).  The
+    header's tensor list is checked against the config (names, order, shapes, n_layers layers)
+    before anything is uploaded, so the device never builds tensor maps over short buffers."""
     from .weights import DeviceWeights, _finish, _to_device_layer
     import torch
 
-    cfg, _, _ = read_header(path)
+    cfg, header, _ = read_header(path)
+    _check_header(path, cfg, header)
     dw = DeviceWeights(cfg, None, [], [], [], [], [], [], None, None, None, None, None)
     cur: dict = {}
     final = None
@@ -157,4 +185,6 @@ def load_checkpoint_to_device(path: str, device="cuda"):
                 dw.ln_attn.append(torch.from_numpy(cur["rms_attn"]).to(device))
                 dw.ln_mlp.append(torch.from_numpy(cur["rms_mlp"]).to(device))
                 cur = {}
+    if len(dw.w_qkv) != cfg.n_layers or dw.w_yes is None:
+        raise ValueError(f"{path}: loaded {len(dw.w_qkv)} of {cfg.n_layers} layers")
     return dw

@@ -516,8 +516,6 @@ int debug_set_attention_trace(unsigned long long* buf, unsigned int cap) {
   return 0;
 }
 
-static int g_att_sms = 0;
-
 template <int DH>
 static int launch_attention_t(const AttnDesc& d, cudaStream_t stream) {
   const int ldq = (d.H + 2 * d.Hkv) * d.dh;
@@ -526,19 +524,18 @@ static int launch_attention_t(const AttnDesc& d, cudaStream_t stream) {
   if (!make_tmap_2d(&tkv, d.qkv, 2, (uint64_t)d.T, (uint64_t)ldq, (uint64_t)ldq, AT_KB, 64, true)) return -3;
   const int ldo = d.H * d.dh;
   if (!make_tmap_2d(&to, d.out, 2, (uint64_t)d.T, (uint64_t)ldo, (uint64_t)ldo, 32, 64, true)) return -3;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_prefix_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, AtCfg<DH>::SMEM);
-    attr_set = true;
+  const int dev = current_device();
+  static bool attr_set[kMaxDevices] = {};
+  if (!attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(attn_prefix_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         AtCfg<DH>::SMEM);
+    if (e != cudaSuccess) return fail(-4, "attention smem attr (device %d): %s", dev, cudaGetErrorString(e));
+    attr_set[dev] = true;
   }
-  if (g_att_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_att_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sm_count(dev);
   const int r = d.H / d.Hkv;
   const int n_units = d.n_work * d.Hkv * ((r + 1) / 2);
-  const int grid = n_units < g_att_sms ? n_units : g_att_sms;
+  const int grid = n_units < sms ? n_units : sms;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(AT_THREADS);

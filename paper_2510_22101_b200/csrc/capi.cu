@@ -38,6 +38,22 @@ bool pdl_enabled() {
   return v == 1;
 }
 
+int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
+int device_sm_count(int dev) {
+  static int sms[kMaxDevices] = {};
+  if (sms[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+    sms[dev] = n;
+  }
+  return sms[dev];
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -135,6 +151,7 @@ struct Workspace {
   int32_t *ids, *pos, *segs, *work, *last_idx;
   float *logits2, *p_yes;
   int* bad;
+  int* verr;         // pf_score under PF_VALIDATE=1: device bounds-check result (launch_validate_packed)
   size_t total;
 };
 
@@ -162,6 +179,7 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   w.logits2 = reinterpret_cast<float*>(take((size_t)n_items * 8));
   w.p_yes = reinterpret_cast<float*>(take((size_t)n_items * 4));
   w.bad = reinterpret_cast<int*>(take(16));
+  w.verr = reinterpret_cast<int*>(take(16));
   w.total = off;
   return w;
 }
@@ -402,6 +420,47 @@ static int check_args(pf_model* m, int T, int n_items, int n_seg, int n_work, vo
   return 0;
 }
 
+static const char* const kFaultNames[] = {"", "token id", "position", "segment", "work tile", "last_idx"};
+
+// Runs the device bounds check into `err` and waits for it; 0 when the batch is valid.
+static int validate_device_sync(const pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
+                                int n_seg, const int32_t* work, int n_work, const int32_t* last_idx, int n_items,
+                                int T, int* err, cudaStream_t st) {
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return fail(-1, "PF_VALIDATE=1 cannot be used while the stream is captured into a graph");
+  int rc = launch_validate_packed(ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, m->d.vocab_size,
+                                  m->d.max_seq, err, st);
+  if (rc) return rc;
+  int h[2] = {0, 0};
+  cudaError_t e = cudaMemcpyAsync(h, err, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(-4, "validate: %s", cudaGetErrorString(e));
+  if (h[0] != 0)
+    return fail(-1, "packed batch invalid: %s at index %d", kFaultNames[h[0] >= 1 && h[0] <= 5 ? h[0] : 0], h[1]);
+  return 0;
+}
+
+static bool validate_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_VALIDATE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+int pf_validate_packed(const pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs, int n_seg,
+                       const int32_t* work, int n_work, const int32_t* last_idx, int n_items, int T, int* err,
+                       pf_stream_t stream) {
+  if (!m) return fail(-1, "null model handle");
+  if (T < 1 || n_items < 1 || n_seg < 1 || n_work < 1 || n_seg > T || n_work > T)
+    return fail(-1, "bad batch sizes T=%d items=%d segs=%d work=%d", T, n_items, n_seg, n_work);
+  if (!ids || !pos || !segs || !work || !last_idx || !err) return fail(-1, "pf_validate_packed: null buffer");
+  return launch_validate_packed(ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, m->d.vocab_size,
+                                m->d.max_seq, err, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int pf_score(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs, int n_seg,
              const int32_t* work, int n_work, const int32_t* last_idx, int n_items, int T,
              void* workspace, size_t ws_bytes, float* logits2, float* p_yes, int* bad_flag,
@@ -410,6 +469,10 @@ int pf_score(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t*
   int rc = check_args(m, T, n_items, n_seg, n_work, workspace, ws_bytes, &need);
   if (rc) return rc;
   Workspace w = layout(m, T, n_items, T, T, static_cast<uint8_t*>(workspace));
+  if (validate_env() &&
+      (rc = validate_device_sync(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, w.verr,
+                                 reinterpret_cast<cudaStream_t>(stream))))
+    return rc;
   return run_forward(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, w, logits2,
                      p_yes, bad_flag, reinterpret_cast<cudaStream_t>(stream));
 }
@@ -425,6 +488,10 @@ int pf_score_capture(pf_model* m, const int32_t* ids, const int32_t* pos, const 
       (cap->out_layer_stride != 0 && cap->out_layer_stride < (long long)cap->n_rows * m->d.d_model))
     return fail(-1, "pf_score_capture: bad capture descriptor");
   Workspace w = layout(m, T, n_items, T, T, static_cast<uint8_t*>(workspace));
+  if (validate_env() &&
+      (rc = validate_device_sync(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, w.verr,
+                                 reinterpret_cast<cudaStream_t>(stream))))
+    return rc;
   return run_forward(m, ids, pos, segs, n_seg, work, n_work, last_idx, n_items, T, w, logits2, p_yes, bad_flag,
                      reinterpret_cast<cudaStream_t>(stream), cap);
 }

@@ -228,6 +228,58 @@ int launch_rope_gather(const int32_t* pos, const float* cos_tab, const float* si
   return e == cudaSuccess ? 0 : fail(-4, "rope_gather launch: %s", cudaGetErrorString(e));
 }
 
+// ---------------------------------------------------------------- packed-batch bounds check
+// Device-side twin of capi.cu validate_packed for batches that are already resident on the device
+// (pf_validate_packed, and pf_score under PF_VALIDATE=1).  One thread per checked element over the
+// concatenated index space [ids | pos | segs | work | last_idx]; the first violation found wins
+// err[0] (code, PF_BAD_* in pf_internal.h) via atomicCAS and records its index in err[1].
+__global__ void __launch_bounds__(256) validate_packed_kernel(
+    const int32_t* __restrict__ ids, const int32_t* __restrict__ pos, const int4* __restrict__ segs, int n_seg,
+    const int4* __restrict__ work, int n_work, const int32_t* __restrict__ last_idx, int n_items, int T,
+    int vocab, int max_seq, int* __restrict__ err) {
+  const long long total = 2LL * T + n_seg + n_work + n_items;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int code = 0;
+    long long idx = i;
+    if (idx < T) {
+      const int v = __ldg(ids + idx);
+      if (v < 0 || v >= vocab) code = PF_BAD_ID;
+    } else if ((idx -= T) < T) {
+      const int v = __ldg(pos + idx);
+      if (v < 0 || v >= max_seq) code = PF_BAD_POS;
+    } else if ((idx -= T) < n_seg) {
+      const int4 g = __ldg(segs + idx);
+      if (g.x < 0 || g.y < 0 || g.z < 0 || g.w < 1 || (long long)g.x + g.y > T || (long long)g.z + g.w > T)
+        code = PF_BAD_SEG;
+    } else if ((idx -= n_seg) < n_work) {
+      const int4 k = __ldg(work + idx);
+      if (k.x < 0 || k.x >= n_seg || k.y < 0 || (long long)k.y * 128 >= __ldg(segs + k.x).w) code = PF_BAD_WORK;
+    } else {
+      idx -= n_work;
+      const int v = __ldg(last_idx + idx);
+      if (v < 0 || v >= T) code = PF_BAD_LAST;
+    }
+    if (code != 0 && atomicCAS(err, 0, code) == 0) err[1] = (int)idx;
+  }
+}
+
+int launch_validate_packed(const int32_t* ids, const int32_t* pos, const int32_t* segs, int n_seg,
+                           const int32_t* work, int n_work, const int32_t* last_idx, int n_items, int T, int vocab,
+                           int max_seq, int* err, cudaStream_t stream) {
+  if (((reinterpret_cast<uintptr_t>(segs) | reinterpret_cast<uintptr_t>(work)) & 15) != 0)
+    return fail(-1, "validate: segs/work must be 16-byte aligned");
+  cudaError_t e = cudaMemsetAsync(err, 0, 2 * sizeof(int), stream);
+  if (e != cudaSuccess) return fail(-4, "validate memset: %s", cudaGetErrorString(e));
+  const long long total = 2LL * T + n_seg + n_work + n_items;
+  const long long blocks = (total + 255) / 256;
+  validate_packed_kernel<<<(unsigned)(blocks < 1184 ? blocks : 1184), 256, 0, stream>>>(
+      ids, pos, reinterpret_cast<const int4*>(segs), n_seg, reinterpret_cast<const int4*>(work), n_work, last_idx,
+      n_items, T, vocab, max_seq, err);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "validate launch: %s", cudaGetErrorString(e));
+}
+
 int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* lo, const float* ss, int ss_ld,
                         const float* g, int d, float eps, float* out, cudaStream_t stream) {
   if (n == 0) return 0;

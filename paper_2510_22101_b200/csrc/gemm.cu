@@ -619,7 +619,6 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
 
 int gemm_smem_bytes() { return GemmCfg<2, EPI_BF16>::SMEM; }
 
-static int g_num_sms = 0;
 static int g_gemm_cg = 0;
 
 int gemm_cta_group() {
@@ -634,15 +633,16 @@ template <int EPI, int CG>
 static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                          const CUtensorMap& td, const GemmArgs& a, cudaStream_t stream) {
   using Cfg = GemmCfg<CG, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  const int dev = current_device();
+  static bool attr_set[kMaxDevices] = {};
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI, CG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    if (e != cudaSuccess) return fail(-4, "gemm smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
+    if (e != cudaSuccess) return fail(-4, "gemm smem attr (device %d): %s", dev, cudaGetErrorString(e));
+    attr_set[dev] = true;
   }
   const int tiles = a.num_m_blk * a.num_n_blk;
-  const int groups = g_num_sms / CG;
+  const int groups = device_sm_count(dev) / CG;
   const int grid = (tiles < groups ? tiles : groups) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -693,11 +693,6 @@ int launch_gemm(const GemmDesc& d, const CUtensorMap* cached_b, cudaStream_t str
     return fail(-2, "gemm: SwiGLU N=%d must be a multiple of %d", d.N, GEMM_BN);
   if (d.epilogue == EPI_ROPE_BF16 && (d.pos == nullptr || d.rope_cos == nullptr))
     return fail(-2, "gemm: RoPE epilogue needs positions and tables");
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   const int cg = gemm_cta_group();
   CUtensorMap ta, tb, tc, td;
   if (!make_tmap_2d(&ta, d.A, 2, d.M, d.K, d.lda, GEMM_BM, GEMM_BK, true)) return -3;

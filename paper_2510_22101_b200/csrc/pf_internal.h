@@ -22,6 +22,13 @@ bool pdl_enabled();
 void set_error(const char* fmt, ...);
 int fail(int code, const char* fmt, ...);
 
+// ---- per-device launch state.  CUDA function attributes (max dynamic smem) and SM counts belong
+// to a device context, so launchers key them by the calling thread's current device (the engine
+// makes the model's device current around every call).
+constexpr int kMaxDevices = 64;
+int current_device();          // cudaGetDevice, clamped to [0, kMaxDevices)
+int device_sm_count(int dev);  // cached per device
+
 // ---- tensor maps (host)
 // 2-D row-major tensor [rows x cols] of `elem_bytes`-sized elements, `ld` elements per row,
 // box = [box_rows x box_cols], 128-byte swizzle when box_cols*elem_bytes == 128.
@@ -89,6 +96,13 @@ int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int att
 int launch_head(const float* resid, const void* rhi, const void* rlo, const int32_t* last_idx, int n_items, int d,
                 const float* final_gamma, const float* w_yes, const float* w_no, float eps,
                 float* logits2, float* p_yes, int* bad_flag, cudaStream_t stream);
+
+// Packed-batch bounds check on the device (elementwise.cu).  err[0] = first violation's PF_BAD_*
+// code (0 = valid), err[1] = its index inside that array.
+enum PackedFault : int { PF_BAD_ID = 1, PF_BAD_POS = 2, PF_BAD_SEG = 3, PF_BAD_WORK = 4, PF_BAD_LAST = 5 };
+int launch_validate_packed(const int32_t* ids, const int32_t* pos, const int32_t* segs, int n_seg,
+                           const int32_t* work, int n_work, const int32_t* last_idx, int n_items, int T, int vocab,
+                           int max_seq, int* err, cudaStream_t stream);
 
 struct AttnDesc {
   const void* qkv;        // [T x (H+2Hkv)*dh] bf16 (RoPE already applied to q, k)

@@ -77,9 +77,15 @@ def prune_mlp_neurons(weights: Weights, keep, w_down_rows=None) -> Weights:
     layers = []
     for l, lw in enumerate(weights.layers):
         idx = _check_keep(keep[l], cfg.d_ff, f"layer {l}")
-        down = lw.W_down[idx] if w_down_rows is None else np.asarray(w_down_rows[l], dtype=np.float32)
-        if down.shape != (k, cfg.d_model):
-            raise ValueError("refit W_down rows must be [k x d_model]")
+        if w_down_rows is None:
+            down = lw.W_down[idx]
+        else:
+            # refit rows are aligned with the caller's keep-set order; neurons are taken in ascending
+            # index order, so reorder the rows by the same permutation
+            down = np.asarray(w_down_rows[l], dtype=np.float32)
+            if down.shape != (k, cfg.d_model):
+                raise ValueError("refit W_down rows must be [k x d_model]")
+            down = down[np.argsort(np.asarray(keep[l], dtype=np.int64), kind="stable")]
         layers.append(replace(lw, W_gate=lw.W_gate[:, idx].copy(), W_up=lw.W_up[:, idx].copy(),
                               W_down=down.copy()))
     return Weights(replace(cfg, d_ff=k), weights.token_embedding, layers, weights.final_norm,

@@ -52,3 +52,49 @@ def test_rejects_corrupt_files(tmp_path):
     (tmp_path / "t.prlk").write_bytes(data[:-8])
     with pytest.raises(ValueError):
         load_checkpoint(str(tmp_path / "t.prlk"))
+
+
+def _rewrite_header(src, dst, edit):
+    """Copy a PRLK file with its header JSON edited (tensor bytes unchanged)."""
+    import json
+    import struct
+
+    data = open(src, "rb").read()
+    n = struct.unpack("<I", data[8:12])[0]
+    header = json.loads(data[12:12 + n])
+    edit(header)
+    hb = json.dumps(header, sort_keys=True).encode()
+    hb += b" " * (-len(hb) % 4)
+    open(dst, "wb").write(data[:4] + struct.pack("<II", 1, len(hb)) + hb + data[12 + n:])
+
+
+def test_header_tensor_list_must_match_config(tmp_path):
+    """the device loader trusted the header's tensor list.  A checkpoint whose
+    list omits a layer or disagrees with the config's shapes is rejected before any upload."""
+    from paper_2510_22101_b200.checkpoint import expected_tensors
+
+    cfg = CONFIGS["TINY_GQA"]
+    good = str(tmp_path / "g.prlk")
+    save_checkpoint(init_weights(cfg, 0), good)
+    assert [(n, tuple(s)) for n, s in read_header(good)[1]["tensors"]] == expected_tensors(cfg)
+    # claims one layer more than it holds
+    _rewrite_header(good, tmp_path / "a.prlk", lambda h: h["config"].update(n_layers=cfg.n_layers + 1))
+    # a layer's W_o listed with a smaller shape (same element count elsewhere would go unnoticed)
+    def shrink(h):
+        for t in h["tensors"]:
+            if t[0] == "layers.1.W_o":
+                t[1] = [t[1][0] // 2, t[1][1] * 2]
+    _rewrite_header(good, tmp_path / "b.prlk", shrink)
+    # the last layer's tensors dropped from the list
+    _rewrite_header(good, tmp_path / "c.prlk",
+                    lambda h: h.update(tensors=[t for t in h["tensors"] if not t[0].startswith("layers.2.")]))
+    for bad in ("a", "b", "c"):
+        with pytest.raises(ValueError):
+            load_checkpoint(str(tmp_path / f"{bad}.prlk"))
+        try:
+            import torch  # noqa: F401
+            from paper_2510_22101_b200.checkpoint import load_checkpoint_to_device
+        except ImportError:
+            continue
+        with pytest.raises(ValueError):
+            load_checkpoint_to_device(str(tmp_path / f"{bad}.prlk"), device="cpu")

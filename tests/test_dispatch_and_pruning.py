@@ -126,6 +126,21 @@ def test_prune_mlp_and_layers_contract():
         PruneRecipe(mlp_sparsity=1.0)
 
 
+def test_refit_rows_follow_the_callers_keep_order():
+    """refit W_down rows aligned with an unsorted keep-set stay paired with their neurons."""
+    cfg = CONFIGS["TINY_GQA"]
+    w = init_weights(cfg, 0)
+    k = kept_width(cfg.d_ff, 0.5)
+    rng = np.random.default_rng(3)
+    keep = [rng.permutation(cfg.d_ff)[:k] for _ in range(cfg.n_layers)]           # unsorted
+    rows = [w.layers[l].W_down[keep[l]] * 2.0 for l in range(cfg.n_layers)]      # aligned with keep
+    pw = prune_mlp_neurons(w, keep, rows)
+    for l in range(cfg.n_layers):
+        order = np.sort(keep[l])
+        np.testing.assert_array_equal(pw.layers[l].W_gate, w.layers[l].W_gate[:, order])
+        np.testing.assert_array_equal(pw.layers[l].W_down, w.layers[l].W_down[order] * 2.0)
+
+
 def test_prune_kv_groups_keeps_gqa_invariant():
     cfg = CONFIGS["C3"].with_(n_layers=1, vocab_size=64)
     w = init_weights(cfg, 0)

@@ -1,0 +1,196 @@
+"""The reference's entry points with the reference's signatures.
+
+CPU part: argument errors the spec names (they are raised before any device work), the host-side
+packed-batch bounds check, the device-weight shape discipline, and the cache of one scorer per
+(weights, device).  GPU part (-m gpu): ``forward_prefill`` / ``forward_with_prefix`` /
+``score_shared_batch(weights, shared)`` against the CPU fp32 oracle's functions of the same names.
+"""
+
+import numpy as np
+import pytest
+
+import oracle.model as OM
+import oracle.prefixcache as OP
+import oracle.scoring as OS
+from paper_2510_22101_b200 import CONFIGS, SharedBatch, init_weights, pack_requests, relevance_score
+from paper_2510_22101_b200.engine import (KVCache, ScoredBatch, forward_prefill, forward_with_prefix,
+                                          score_shared_batch, validate_packed)
+from tests.synth import make_shared
+
+TOL_P = 1e-2
+
+
+# ----------------------------------------------------------------------------- CPU: errors
+def test_forward_prefill_rejects_empty_and_over_length():
+    w = init_weights(CONFIGS["TINY"], 0)
+    with pytest.raises(ValueError):
+        forward_prefill(w, [])
+    with pytest.raises(ValueError):
+        forward_prefill(w, [16] * (w.config.max_seq + 1))
+
+
+def test_forward_with_prefix_errors():
+    w = init_weights(CONFIGS["TINY"], 0)
+    cfg = w.config
+    kv = KVCache(tuple([16] * 10), cfg.n_layers)
+    with pytest.raises(ValueError, match="empty suffix"):
+        forward_with_prefix(w, kv, [])
+    with pytest.raises(ValueError, match="max_seq"):
+        forward_with_prefix(w, kv, [17] * (cfg.max_seq - 9))
+    with pytest.raises(ValueError, match="layers"):
+        forward_with_prefix(w, KVCache(kv.tokens, cfg.n_layers + 1), [17])
+    with pytest.raises(TypeError):
+        forward_with_prefix(w, list(kv.tokens), [17])
+    assert kv.seq_len == 10
+
+
+def test_score_shared_batch_argument_errors():
+    w = init_weights(CONFIGS["TINY"], 0)
+    with pytest.raises(ValueError):
+        score_shared_batch(w, [])
+    with pytest.raises(ValueError):
+        score_shared_batch(w, SharedBatch([16] * 2000, [[17] * 100]))
+    with pytest.raises(TypeError):
+        score_shared_batch(object(), SharedBatch([16], [[17]]))
+
+
+def test_scored_batch_is_the_spec_list_of_logits():
+    res = ScoredBatch(np.array([[2.0, 0.0], [0.0, 0.0]], np.float32), np.array([0.880797, 0.5], np.float32))
+    assert len(res) == 2
+    assert [round(relevance_score(l).p_yes, 6) for l in res] == [0.880797, 0.5]
+    assert np.array_equal(res[0], [2.0, 0.0])
+
+
+def _good():
+    rng = np.random.default_rng(0)
+    return pack_requests([make_shared(rng, 20, [5, 130, 7], "spread"), make_shared(rng, 0, [9], "spread")])
+
+
+@pytest.mark.parametrize("field,index,value", [
+    ("ids", (0,), 40000), ("ids", (3,), -1), ("pos", (2,), 2048), ("pos", (1,), -5),
+    ("segs", (1, 3), 0), ("segs", (1, 2), 10 ** 6), ("segs", (0, 1), -1),
+    ("work", (0, 0), 99), ("work", (0, 1), 7), ("last_idx", (1,), 10 ** 6), ("last_idx", (0,), -1)])
+def test_host_validation_rejects_each_malformed_field(field, index, value):
+    cfg = CONFIGS["TINY"]
+    validate_packed(_good(), cfg)
+    pk = _good()
+    getattr(pk, field)[index] = value
+    with pytest.raises(ValueError):
+        validate_packed(pk, cfg)
+
+
+def test_device_weight_shape_discipline():
+    """a layer list shorter than n_layers or a tensor smaller than its config shape is
+    rejected before pf_model_create builds tensor maps over it."""
+    torch = pytest.importorskip("torch")
+    from paper_2510_22101_b200.engine import check_device_weights
+    from paper_2510_22101_b200.weights import to_device
+
+    cfg = CONFIGS["TINY"]
+    dw = to_device(init_weights(cfg, 0), "cpu")
+    check_device_weights(dw, torch.device("cpu"))
+    dw.w_down = dw.w_down[:-1]
+    with pytest.raises(ValueError, match="layers"):
+        check_device_weights(dw, torch.device("cpu"))
+    dw = to_device(init_weights(cfg, 0), "cpu")
+    dw.w_o[1] = dw.w_o[1][:, :128].contiguous()
+    with pytest.raises(ValueError, match="w_o"):
+        check_device_weights(dw, torch.device("cpu"))
+
+
+# ----------------------------------------------------------------------------- GPU: parity
+def _oracle_logits2(ow, prefix, suffix):
+    if prefix:
+        _, kv = OM.forward_prefill(ow, prefix)
+        logits, _ = OM.forward_with_prefix(ow, kv, suffix)
+    else:
+        logits, _ = OM.forward_prefill(ow, suffix)
+    return np.array([logits[1], logits[2]], dtype=np.float64)
+
+
+@pytest.mark.gpu
+def test_forward_prefill_and_with_prefix_match_oracle():
+    cfg = CONFIGS["TINY_GQA"]
+    w, ow = init_weights(cfg, 0), OM.init_weights(cfg, 0)
+    rng = np.random.default_rng(40)
+    toks = [3] + [int(x) for x in rng.integers(16, cfg.vocab_size, 39)]
+    full, kv_full, cap = forward_prefill(w, toks)
+    assert cap is None and kv_full.seq_len == 40
+    ref = _oracle_logits2(ow, [], toks)
+    assert np.max(np.abs(full - ref)) < 5e-2
+    # random 40-token prompt split at 25: prefix cache + suffix == full pass
+    _, kv25, _ = forward_prefill(w, toks[:25])
+    split, kv_ext, = forward_with_prefix(w, kv25, toks[25:])[:2]
+    assert kv_ext.seq_len == 40 and kv_ext.tokens == kv_full.tokens
+    np.testing.assert_allclose(split, full, rtol=0, atol=1e-6)
+    p = relevance_score(split).p_yes
+    p_ref = OS.relevance_score(np.concatenate([[0.0], ref]))[0]
+    assert abs(p - p_ref) <= TOL_P
+    # two suffixes under one prefix cache: each equals its own full pass
+    for suf in ([17, 18, 19], [int(x) for x in rng.integers(16, cfg.vocab_size, 60)]):
+        a, _ = forward_with_prefix(w, kv25, suf)
+        b, _, _ = forward_prefill(w, toks[:25] + suf)
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-6)
+    # single token: finite logits, cache seq_len 1
+    one, kv1, _ = forward_prefill(w, [5])
+    assert np.all(np.isfinite(one)) and kv1.seq_len == 1
+
+
+@pytest.mark.gpu
+def test_forward_prefill_capture_matches_oracle():
+    cfg = CONFIGS["TINY_GQA"]
+    w, ow = init_weights(cfg, 0), OM.init_weights(cfg, 0)
+    rng = np.random.default_rng(41)
+    toks = [int(x) for x in rng.integers(16, cfg.vocab_size, 50)]
+    logits, kv, cap = forward_prefill(w, toks, capture=True)
+    assert cap.shape == (cfg.n_layers, 50, cfg.d_model)
+    _, _, ref = OM.forward_prefill(ow, toks, capture=True)
+    for l in range(cfg.n_layers):
+        r = np.asarray(ref[l], dtype=np.float64)
+        err = np.linalg.norm(cap[l] - r) / np.linalg.norm(r)
+        assert err < 2e-2, (l, err)
+
+
+@pytest.mark.gpu
+def test_score_shared_batch_takes_weights_and_caches_one_scorer():
+    from paper_2510_22101_b200.engine import PrefillScorer, scorer_for
+    from paper_2510_22101_b200.weights import to_device
+
+    cfg = CONFIGS["TINY"]
+    w, ow = init_weights(cfg, 0), OM.init_weights(cfg, 0)
+    rng = np.random.default_rng(42)
+    prompts = [[3] + [int(x) for x in rng.integers(16, cfg.vocab_size, 30)]] * 1
+    prompts = [prompts[0] + [int(x) for x in rng.integers(16, cfg.vocab_size, n)] for n in (5, 40, 1, 77)]
+    sb = OP.split_shared_prefix(prompts)
+    ref = [OS.relevance_score(l)[0] for l in OP.score_shared_batch(ow, sb)]
+    shared = SharedBatch(sb.prefix_tokens, sb.suffixes)
+    a = score_shared_batch(w, shared)
+    got = [relevance_score(l).p_yes for l in a]          # the reference caller's loop, unchanged
+    assert np.max(np.abs(np.array(got) - ref)) <= TOL_P
+    assert scorer_for(w) is scorer_for(w)                 # one replica per (weights, device)
+    b = score_shared_batch(to_device(w, "cuda"), shared)
+    c = score_shared_batch(PrefillScorer(w), shared)
+    np.testing.assert_array_equal(a.logits2, b.logits2)
+    np.testing.assert_array_equal(a.logits2, c.logits2)
+    # batch of 1 == forward_prefill on the full prompt
+    one = score_shared_batch(w, SharedBatch(prompts[1][:-1], [prompts[1][-1:]]))
+    fp, _, _ = forward_prefill(w, prompts[1])
+    np.testing.assert_array_equal(one[0], fp)
+
+
+@pytest.mark.gpu
+def test_device_bounds_check_rejects_malformed_device_batches():
+    """pf_validate_packed on device-resident inputs (the pf_score path trusts its pointers)."""
+    from paper_2510_22101_b200.engine import DevicePacked, PrefillScorer
+
+    scorer = PrefillScorer(init_weights(CONFIGS["TINY"], 0))
+    good = _good()
+    scorer.validate_device(DevicePacked(good, scorer.device))
+    for field, index, value in [("ids", (0,), 40000), ("pos", (2,), 2048), ("segs", (1, 3), 0),
+                                ("work", (0, 0), 99), ("last_idx", (1,), 10 ** 6)]:
+        pk = _good()
+        getattr(pk, field)[index] = value
+        with pytest.raises(ValueError, match="invalid"):
+            scorer.validate_device(DevicePacked(pk, scorer.device))
+    res = scorer.score_device(DevicePacked(good, scorer.device), validate=True)
+    assert res[1].shape[0] == good.n_items
