@@ -418,18 +418,44 @@ def run_ours(args):
 
 
 # ----------------------------------------------------------------------------- C5 mixed load
-def c5_request(rng, cfg, prefix_len=64):
-    """items ~U{10..500}, item tokens ~U{64..1024}, 64-token query prefix."""
-    from paper_2510_22101_b200 import SharedBatch
+C5_QUERY_WORDS = 48        # <|sys|>...(13) + <|q|> 48 words <|/q|> + <|meta|> = a 64-token shared prefix
+C5_ITEM_OVERHEAD = 12      # item tokens = 12 + description words (metadata 9 after <|meta|>, desc tags 2, <|ans|>)
 
-    n = int(rng.integers(10, 501))
-    prefix = [3] + [int(x) for x in rng.integers(16, cfg.vocab_size, prefix_len - 1)]
-    sufs = []
-    for s_len in rng.integers(64, 1025, n):
-        suf = rng.integers(16, cfg.vocab_size, int(s_len)).astype(np.int64)
-        suf[-1] = 11
-        sufs.append(suf.tolist())
-    return SharedBatch(prefix, sufs)
+
+class C5Workload:
+    """SURVEY.md §8d C5 as text requests for the serving wrapper: per request items ~U{10..500}, item
+    prompts of ~U{64..1024} tokens after the shared prefix, a 64-token prefix (system prompt + query).
+    Words are synthetic ("w<number>", one hashed token each).  A pool of item lists is generated once;
+    every issued request gets a fresh query text (so no request hits the score cache) and its own
+    item ids."""
+
+    def __init__(self, seed: int, pool: int):
+        from paper_2510_22101_b200.serving import JobItem
+
+        rng = np.random.default_rng(seed)
+        self.rng = rng
+        words = np.array([f"w{i}" for i in range(50000)])
+        self.words = words
+        self.pool = []
+        for r in range(pool):
+            n = int(rng.integers(10, 501))
+            lens = rng.integers(64, 1025, n)
+            items = [JobItem(f"p{r}i{i}", "senior engineer", "acme corp", "berlin", "full_time", True,
+                             " ".join(words[rng.integers(0, len(words), int(S) - C5_ITEM_OVERHEAD)]))
+                     for i, S in enumerate(lens)]
+            self.pool.append((items, lens))
+        self.k = 0
+
+    def next(self, arrival=None):
+        from paper_2510_22101_b200.serving import JobItem, Query, ScoreRequest
+
+        items, lens = self.pool[self.k % len(self.pool)]
+        k = self.k
+        self.k += 1
+        q = Query(f"q{k}", " ".join(self.words[self.rng.integers(0, len(self.words), C5_QUERY_WORDS)]))
+        its = [JobItem(f"r{k}-{it.id}", it.title, it.company, it.location, it.employment_type, it.remote_eligible,
+                       it.description) for it in items]
+        return ScoreRequest(q, its, f"req{k}", arrival), len(items), int(64 + lens.sum())
 
 
 def nearest_rank(sorted_vals, q):
@@ -441,88 +467,112 @@ def nearest_rank(sorted_vals, q):
 
 
 def run_load(args):
-    """Open-loop Poisson load on one GPU: requests arrive at seeded exponential
-    gaps; a serving loop packs every request that has arrived (up to a token budget) into one
-    pf_score call; latency = completion - arrival (wall clock, includes packing, H2D, D2H)."""
+    """C5: open-loop Poisson load through the serving wrapper
+    (``ScoringService.submit``: Eq-1 assembly, truncation, native tokenizer + packer, cache) onto a
+    ``ReplicaPool`` of one replica per visible GPU (one process, one worker thread per GPU, batched
+    and pipelined launches, large requests item-split across replicas).  Capacity is measured
+    closed-loop first; each load point then issues requests at seeded exponential gaps for
+    max(--load-seconds, --load-requests / rate), discards the first --load-warmup-s seconds
+    (SPEC.md:789), and reports nearest-rank percentiles of arrival -> response latency."""
+    import threading
+
     import torch
 
-    from paper_2510_22101_b200 import CONFIGS, concat_packed, init_device_weights, pack_requests
+    from paper_2510_22101_b200 import CONFIGS, init_device_weights
     from paper_2510_22101_b200.engine import PrefillScorer
+    from paper_2510_22101_b200.replicas import ReplicaPool
+    from paper_2510_22101_b200.serving import ScoreCache, ScoringService
 
     cfg = CONFIGS["C4"]
-    torch.cuda.set_device(0)
-    scorer = PrefillScorer(init_device_weights(cfg, 0, "cuda"), device="cuda")
-    rng = np.random.default_rng(args.seed)
-    pool = [c5_request(rng, cfg) for _ in range(args.load_pool)]
-    items_per_req = float(np.mean([r.n_items for r in pool]))
-    tok_per_req = float(np.mean([len(r.prefix_tokens) + sum(len(s) for s in r.suffixes) for r in pool]))
-    budget = args.load_token_budget
-    # each request is packed once when it arrives (off the serving loop, as a front end would);
-    # a launch only joins the arrived requests' arrays (concat_packed, ~1 ms per launch)
-    t0 = time.perf_counter()
-    pre = [pack_requests([r], cfg.max_seq) for r in pool]
-    pack_ms_per_req = (time.perf_counter() - t0) * 1e3 / len(pool)
+    n_dev = min(args.gpus, torch.cuda.device_count())
+    scorers = [PrefillScorer(init_device_weights(cfg, 0, f"cuda:{i}"), device=f"cuda:{i}") for i in range(n_dev)]
+    pool = ReplicaPool(scorers, token_budget=args.load_token_budget,
+                       max_shard_items=args.c5_shard_items if args.c5_shard_items > 0 else None)
+    svc = ScoringService(pool, model_version="c4-seed0", cache=ScoreCache(), workers=args.c5_workers,
+                         model_config=cfg)
+    wl = C5Workload(args.seed, args.load_pool)
+    items_per_req = float(np.mean([len(it) for it, _ in wl.pool]))
+    tok_per_req = float(np.mean([64 + l.sum() for _, l in wl.pool]))
 
-    def serve(batch_idx):
-        return scorer.score_packed(concat_packed([pre[k] for k in batch_idx]))
+    def issue(n):
+        out = []
+        for _ in range(n):
+            req, n_items, _ = wl.next()
+            out.append((svc.submit(req), n_items))
+        return out
 
-    for k in range(3):      # warm-up (kernel attributes, workspace growth)
-        serve([k])
-    # capacity: the whole pool back to back, packed up to the token budget
-    torch.cuda.synchronize()
+    for f, _ in issue(3):          # warm-up: kernel attributes, workspaces, pinned pools
+        f.result()
+    clocks = ClockSampler(list(range(n_dev)))
+    # capacity: a closed-loop burst (every request submitted at once, scored back to back)
+    n_cap = max(len(wl.pool), 4 * n_dev)
     t0 = time.perf_counter()
-    i = 0
-    while i < len(pool):
-        batch, toks = [], 0
-        while i < len(pool) and (not batch or toks + tok_per_req <= budget):
-            batch.append(i); toks += tok_per_req; i += 1
-        serve(batch)
+    futs = issue(n_cap)
+    for f, _ in futs:
+        f.result()
     cap_s = time.perf_counter() - t0
-    capacity = sum(r.n_items for r in pool) / cap_s
+    capacity = sum(n for _, n in futs) / cap_s
 
     runs = []
     for frac in args.load_fracs:
-        rate = frac * capacity / items_per_req             # requests/s
+        rate = frac * capacity / items_per_req               # requests/s
+        n_req = int(max(args.load_requests, rate * args.load_seconds) + rate * args.load_warmup_s)
         arng = np.random.default_rng(args.seed + int(frac * 1000))
-        n_req = max(8, int(rate * args.load_seconds))
-        arrivals = np.cumsum(arng.exponential(1.0 / rate, n_req))
-        reqs = [pool[k % len(pool)] for k in range(n_req)]
-        req_pool = [k % len(pool) for k in range(n_req)]
-        done = np.zeros(n_req)
-        start = time.perf_counter()
-        nxt = 0
-        queue = []
-        while nxt < n_req or queue:
-            now = time.perf_counter() - start
-            while nxt < n_req and arrivals[nxt] <= now:
-                queue.append(nxt); nxt += 1
-            if not queue:
-                time.sleep(max(0.0, min(arrivals[nxt] - now, 0.01)))
-                continue
-            batch, toks = [], 0
-            while queue and (not batch or toks + tok_per_req <= budget):
-                batch.append(queue.pop(0)); toks += tok_per_req
-            serve([req_pool[k] for k in batch])
-            t_done = time.perf_counter() - start
-            for k in batch:
-                done[k] = t_done
-        lat = sorted(((done - arrivals) * 1e3).tolist())
-        wall = done.max() - arrivals[0]
-        runs.append({"offered_frac": frac, "offered_items_per_s": frac * capacity,
-                     "achieved_items_per_s": sum(r.n_items for r in reqs) / wall,
-                     "requests": n_req, "p50_ms": nearest_rank(lat, 50), "p90_ms": nearest_rank(lat, 90),
-                     "p95_ms": nearest_rank(lat, 95), "p99_ms": nearest_rank(lat, 99)})
+        gaps = arng.exponential(1.0 / rate, n_req)
+        reqs = [wl.next() for _ in range(n_req)]           # generated before the clock starts
+        recs = [None] * n_req
+        start = time.monotonic() + 0.05
+        arrivals = start + np.cumsum(gaps)
+
+        def generator():
+            for k in range(n_req):
+                d = arrivals[k] - time.monotonic()
+                if d > 0:
+                    time.sleep(d)
+                req, n_items, _ = reqs[k]
+                req.arrival = float(arrivals[k])
+                recs[k] = (svc.submit(req), n_items)
+
+        g = threading.Thread(target=generator)
+        g.start()
+        g.join()
+        lat, lat_all, items_done, t_last = [], [], 0, start
+        for k in range(n_req):
+            fut, n_items = recs[k]
+            resp = fut.result()
+            ms = resp.timings_ms["total"]
+            lat_all.append(ms)
+            if arrivals[k] - start >= args.load_warmup_s:
+                lat.append(ms)
+                items_done += n_items
+        done_t = time.monotonic()
+        measured = [k for k in range(n_req) if arrivals[k] - start >= args.load_warmup_s]
+        window = done_t - arrivals[measured[0]] if measured else 1.0
+        lat.sort()
+        runs.append({"offered_frac": frac, "offered_items_per_s": frac * capacity, "requests_issued": n_req,
+                     "requests_measured": len(lat), "warmup_s": args.load_warmup_s,
+                     "achieved_items_per_s": items_done / window,
+                     "p50_ms": nearest_rank(lat, 50), "p90_ms": nearest_rank(lat, 90),
+                     "p95_ms": nearest_rank(lat, 95), "p99_ms": nearest_rank(lat, 99), "max_ms": lat[-1] if lat else None})
+    clk = clocks.stop()
+    met = svc.metrics()
+    stats = pool.stats()
+    svc.close()
+    pool.close()
     line = {
-        "metric": METRIC, "value": runs[-1]["achieved_items_per_s"], "unit": "items/s", "n_gpus": 1,
-        "steps": sum(r["requests"] for r in runs), "warmup": 3, "ms_per_step": None,
+        "metric": METRIC, "value": capacity, "unit": "items/s", "n_gpus": n_dev,
+        "steps": sum(r["requests_issued"] for r in runs), "warmup": 3, "ms_per_step": None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic C5 mix (seeded): items ~U{10..500}, item tokens ~U{64..1024}, prefix 64; Poisson arrivals",
-        "config": {"workload": "C5 mixed load on the C4 model (1.7B-shaped, pruned 40%)",
+        "data": ("synthetic C5 text requests (seeded): items ~U{10..500}, item prompts ~U{64..1024} tokens, "
+                 "64-token prefix; Poisson arrivals; random-init bf16 weights"),
+        "config": {"workload": "C5 mixed load on the C4 model (1.7B-shaped, pruned 40%) through ScoringService",
                    "mean_items_per_request": items_per_req, "mean_tokens_per_request": tok_per_req,
-                   "token_budget_per_launch": budget, "latency": "wall clock, arrival -> scores on host",
-                   "host_pack_ms_per_request": pack_ms_per_req,
-                   "packing": "per request at arrival (pack_requests), joined per launch (concat_packed)"},
-        "capacity_items_per_s": capacity, "load_runs": runs,
+                   "replicas": n_dev, "token_budget_per_launch": args.load_token_budget,
+                   "shard_items": args.c5_shard_items, "handler_workers": args.c5_workers,
+                   "latency": "arrival -> ScoreResponse (Eq-1 assembly, tokenize, pack, H2D, forward, D2H, rank)",
+                   "value": "closed-loop capacity, items/s over all replicas"},
+        "capacity_items_per_s": capacity, "load_runs": runs, "clocks": clk,
+        "service_metrics": met, "replica_stats": stats,
     }
     print(json.dumps(line), flush=True)
 
@@ -537,6 +587,10 @@ def main():
     ap.add_argument("--seed", type=int, default=5)
     ap.add_argument("--load-pool", type=int, default=24)
     ap.add_argument("--load-seconds", type=float, default=20.0)
+    ap.add_argument("--load-requests", type=int, default=300, help="C5: measured requests per load point (min)")
+    ap.add_argument("--load-warmup-s", type=float, default=5.0, help="C5: discarded seconds per load point")
+    ap.add_argument("--c5-shard-items", type=int, default=0, help="C5: item-split requests above this many items")
+    ap.add_argument("--c5-workers", type=int, default=8, help="C5: service handler threads")
     ap.add_argument("--load-fracs", type=float, nargs="+", default=[0.5, 0.8])
     ap.add_argument("--load-token-budget", type=int, default=262144)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -544,7 +598,7 @@ def main():
     ap.add_argument("--ref-items", type=int, default=8, help="items per reference step (one shared prefix per step)")
     ap.add_argument("--no-graph", action="store_true", help="launch pf_score directly instead of graph replay")
     args = ap.parse_args()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.config != "C5":
         sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)

@@ -222,7 +222,8 @@ class PrefillScorer:
         if bad is None:
             bad = self._state(stream).bad
         if check:
-            bad.zero_() if stream is None else bad.fill_(0)
+            with torch.cuda.stream(self._torch_stream(stream)):
+                bad.zero_()
         with self.device_guard():
             rc = self.lib.pf_score(self.handle, _ptr(dp.ids), _ptr(dp.pos), _ptr(dp.segs), len(pk.segs),
                                    _ptr(dp.work), len(pk.work), _ptr(dp.last_idx), n, pk.T,

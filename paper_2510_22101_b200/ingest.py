@@ -92,13 +92,26 @@ def encode_batch(texts: Sequence[str], vocab: Vocab = DEFAULT_VOCAB, n_threads: 
 def pack_token_lists_native(requests: Sequence[Sequence[Sequence[int]]], max_seq: int = 2048) -> PackedBatch:
     """requests[r] = the token lists of request r (one per item); split_shared_prefix + packing in
     C++.  Same PackedBatch as prefixcache.pack_requests([split_shared_prefix(l) for l in requests])."""
-    lib = _lib.load()
     lists = [np.asarray(l, dtype=np.int32) for req in requests for l in req]
     begin = np.zeros(len(requests) + 1, dtype=np.int32)
     np.cumsum([len(req) for req in requests], out=begin[1:])
     loffs = np.zeros(len(lists) + 1, dtype=np.int64)
     np.cumsum([len(l) for l in lists], out=loffs[1:])
     flat = np.concatenate(lists) if lists else np.zeros(0, np.int32)
+    return pack_flat_native(flat, loffs, begin, max_seq)
+
+
+def pack_flat_native(flat: np.ndarray, loffs: np.ndarray, begin: np.ndarray | None = None,
+                     max_seq: int = 2048) -> PackedBatch:
+    """The same from flat arrays (what encode_batch_arrays returns): token list i is
+    flat[loffs[i]:loffs[i+1]]; request r owns lists begin[r]..begin[r+1]-1 (default: one request)."""
+    lib = _lib.load()
+    flat = np.ascontiguousarray(flat, dtype=np.int32)
+    loffs = np.ascontiguousarray(loffs, dtype=np.int64)
+    if begin is None:
+        begin = np.array([0, len(loffs) - 1], dtype=np.int32)
+    begin = np.ascontiguousarray(begin, dtype=np.int32)
+    requests = [range(int(begin[r]), int(begin[r + 1])) for r in range(len(begin) - 1)]
     T, S, N = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     _lib.check(lib.pf_pack_sizes(loffs.ctypes.data, begin.ctypes.data, len(requests), ctypes.byref(T),
                                  ctypes.byref(S), ctypes.byref(N)))

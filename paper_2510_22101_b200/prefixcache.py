@@ -69,6 +69,22 @@ def throughput_gain(n_query_tokens: int, n_item_tokens: int) -> float:
     return 1.0 + n_query_tokens / n_item_tokens
 
 
+def request_flops(cfg, prefix_len: int, suffix_lens: Sequence[int], shared: bool = True) -> float:
+    """Algorithmic FLOPs of scoring one request (SPEC.md:295 work accounting):
+    L * [tokens * linear_flops_per_token + 4*H*dh * causal (q, k) pairs] at true widths.
+    ``shared``: the prefix is computed once and every suffix attends to it (score_shared_batch);
+    otherwise every item is an independent full pass over prefix + suffix (forward_prefill)."""
+    P = float(prefix_len)
+    S = np.asarray(suffix_lens, dtype=np.float64)
+    if shared:
+        tokens = P + S.sum()
+        pairs = P * (P + 1) / 2 + np.sum(S * P + S * (S + 1) / 2)
+    else:
+        tokens = np.sum(P + S)
+        pairs = np.sum((P + S) * (P + S + 1) / 2)
+    return float(cfg.n_layers * (tokens * cfg.linear_flops_per_token() + 4 * cfg.n_heads * cfg.d_head * pairs))
+
+
 @dataclass
 class AttentionPartial:
     """output [heads x S x d_head], lse [heads x S]."""

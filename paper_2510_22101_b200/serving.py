@@ -260,74 +260,299 @@ class ScoreResponse:
 
 
 class ScoringService:
-    """handle_score_request over a device scorer (``score_packed(PackedBatch) ->
-    ScoredBatch``: a PrefillScorer, or a dispatcher over several replicas)."""
+    """handle_score_request with the spec's concurrency model.
+
+    * ``submit(req) -> Future[ScoreResponse]`` never blocks the caller.  Admission goes through the
+      token-bucket shaper under one lock (the spec's "serializes admissions through one queue");
+      a deferred request waits in a timer queue served by one admission thread, not in a handler.
+    * Admitted requests run on a pool of ``workers`` handler threads: PID depth, cache lookups,
+      Eq-1 assembly, truncation, native tokenization and packing.  The packed request then goes to
+      the scorer: a ``ReplicaPool`` (asynchronous, batched and pipelined across GPU replicas) or
+      any object with ``score_packed(PackedBatch) -> ScoredBatch`` (called on the handler thread).
+    * The cache is guarded by one lock (a lookup moves the LRU position, so reads write too).
+    * One metrics loop owns the PID: every ``pid_interval`` s it feeds the p95 latency of the
+      requests completed in the last ``window_s`` s (SPEC.md:711) to ``PidController.update``;
+      handlers read ``pid.depth`` (an int, read atomically).
+    * ``handle_score_request(req)`` is the synchronous form: ``submit(req).result()``.
+
+    Cache tolerance ("a hit returns exactly the value the model would produce"): a
+    device score depends on its item's prompt only up to bf16 rounding of how the co-batched items
+    split the shared prefix, so a fresh score may differ from a cached one in the low bits.  With
+    ``shadow_rate`` > 0 (test mode) that fraction of hits is re-scored with the misses and the
+    difference is checked against ``shadow_tol`` (1e-2, the parity contract); ``metrics()``
+    reports the checks."""
 
     def __init__(self, scorer, model_version: str, vocab: ingest.Vocab = ingest.DEFAULT_VOCAB,
                  cache: ScoreCache | None = None, pid: PidController | None = None,
                  shaper: TokenBucketShaper | None = None, token_budget: int = 2048, max_seq: int = 2048,
-                 clock: Callable[[], float] = time.monotonic):
+                 clock: Callable[[], float] = time.monotonic, workers: int = 8, target_p95_ms: float = 500.0,
+                 pid_interval: float = 1.0, window_s: float = 10.0, shadow_rate: float = 0.0,
+                 shadow_tol: float = 1e-2, model_config=None, seed: int = 0):
+        import threading
+
         self.scorer, self.model_version, self.vocab = scorer, model_version, vocab
         self.cache = cache if cache is not None else ScoreCache()
         self.pid, self.shaper = pid, shaper
         self.token_budget, self.max_seq, self.clock = token_budget, max_seq, clock
+        self.workers, self.target_p95_ms = int(workers), float(target_p95_ms)
+        self.pid_interval, self.window_s = float(pid_interval), float(window_s)
+        self.shadow_rate, self.shadow_tol = float(shadow_rate), float(shadow_tol)
+        self.model_config = model_config if model_config is not None else getattr(scorer, "config", None)
+        self._rng = np.random.default_rng(seed)
         self.model_calls = self.items_scored = 0
+        self._flops_shared = self._flops_indep = 0.0
+        self._shadow = {"checked": 0, "max_abs_diff": 0.0, "violations": 0}
+        self._lock = threading.Lock()          # cache, counters, latency log
+        self._adm_lock = threading.Lock()      # shaper: admissions serialized
+        self._lat: list = []                   # (t_done, total_ms) of completed requests
+        self._item_log: list = []              # (t_done, n_items scored by the model)
+        self._pool = None
+        self._timer = None
+        self._metrics_thread = None
+        self._closed = False
 
-    def handle_score_request(self, req: ScoreRequest) -> ScoreResponse:
+    # ------------------------------------------------------------------ threads
+    def _ensure_threads(self):
+        import heapq
+        import threading
+        from concurrent.futures import ThreadPoolExecutor
+
+        if self._pool is not None:
+            return
+        with self._adm_lock:
+            if self._pool is not None:
+                return
+            self._heap: list = []
+            self._heap_cv = threading.Condition()
+            self._heapq = heapq
+
+            def admission_loop():
+                while True:
+                    with self._heap_cv:
+                        while not self._heap and not self._closed:
+                            self._heap_cv.wait()
+                        if self._closed and not self._heap:
+                            return
+                        t_adm, k, item = self._heap[0]
+                        wait = t_adm - self.clock()
+                        if wait > 0:
+                            self._heap_cv.wait(timeout=wait)
+                            continue
+                        heapq.heappop(self._heap)
+                    self._pool.submit(self._run, *item)
+
+            self._timer = threading.Thread(target=admission_loop, name="shaper-admission", daemon=True)
+            self._pool = ThreadPoolExecutor(max_workers=self.workers, thread_name_prefix="score-handler")
+            self._timer.start()
+            if self.pid is not None and self.pid_interval > 0:
+                self._metrics_thread = threading.Thread(target=self._metrics_loop, name="metrics-pid", daemon=True)
+                self._metrics_thread.start()
+
+    def close(self):
+        self._closed = True
+        if self._pool is not None:
+            with self._heap_cv:
+                self._heap_cv.notify_all()
+            self._timer.join(timeout=5)
+            self._pool.shutdown(wait=True)
+            if self._metrics_thread is not None:
+                self._metrics_thread.join(timeout=5)
+
+    def _metrics_loop(self):
+        t_prev = self.clock()
+        while not self._closed:
+            time.sleep(self.pid_interval)
+            now = self.clock()
+            p95 = self.p95_ms(now)
+            if p95 is not None:
+                self.pid.update(p95, self.target_p95_ms, max(now - t_prev, 1e-6))
+            t_prev = now
+
+    # ------------------------------------------------------------------ request path
+    def submit(self, req: ScoreRequest):
+        from concurrent.futures import Future
+
+        self._ensure_threads()
+        fut: Future = Future()
         t0 = self.clock()
         arrival = req.arrival if req.arrival is not None else t0
-        admit = self.shaper.admit(arrival) if self.shaper else arrival
-        if admit > t0:
-            time.sleep(admit - t0)
+        with self._adm_lock:
+            admit = self.shaper.admit(arrival) if self.shaper else arrival
+        if admit > self.clock():
+            with self._heap_cv:
+                self._heapq.heappush(self._heap, (admit, id(fut), (req, t0, arrival, fut)))
+                self._heap_cv.notify()
+        else:
+            self._pool.submit(self._run, req, t0, arrival, fut)
+        return fut
+
+    def handle_score_request(self, req: ScoreRequest) -> ScoreResponse:
+        return self.submit(req).result()
+
+    def _run(self, req, t0, arrival, fut):
+        try:
+            self._prepare(req, t0, arrival, fut)
+        except BaseException as e:       # pragma: no cover - surfaced to the caller
+            if not fut.done():
+                fut.set_exception(e)
+
+    def _prepare(self, req, t0, arrival, fut):
         t_admit = self.clock()
         depth = self.pid.depth if self.pid else len(req.items)
         cands, unscored = list(req.items[:depth]), [it.id for it in req.items[depth:]]
         qh = query_hash(req.query.text)
-        scores, misses, errors = {}, [], []
-        for it in cands:
-            p = self.cache.lookup((self.model_version, qh, it.id), t_admit)
-            if p is None:
-                misses.append(it)
-            else:
-                scores[it.id] = (p, "cache")
-        t_tok = t_pre = 0.0
-        if misses:
-            t1 = self.clock()
-            prompts, ok = [], []
-            for it in misses:
-                try:
-                    prompts.append(truncate_description(assemble_prompt(req.query, it), self.token_budget,
-                                                        self.vocab).full_prompt())
-                    ok.append(it)
-                except PromptBudgetError as e:          # per-item rejection (SPEC.md:697)
-                    errors.append({"item_id": it.id, "error": str(e)})
-            token_lists = ingest.encode_batch(prompts, self.vocab) if prompts else []
-            t2 = self.clock()
-            t_tok = t2 - t1
-            if token_lists:
-                packed = ingest.pack_token_lists_native([token_lists], self.max_seq)
-                res = self.scorer.score_packed(packed)
+        scores, misses, errors, shadow = {}, [], [], []
+        with self._lock:
+            for it in cands:
+                p = self.cache.lookup((self.model_version, qh, it.id), t_admit)
+                if p is None:
+                    misses.append(it)
+                else:
+                    scores[it.id] = (p, "cache")
+                    if self.shadow_rate > 0 and self._rng.random() < self.shadow_rate:
+                        shadow.append(it)
+        ctx = {"req": req, "t0": t0, "arrival": arrival, "t_admit": t_admit, "depth": depth, "qh": qh,
+               "scores": scores, "unscored": unscored, "errors": errors, "ok": [], "shadow": 0,
+               "t_tok": 0.0, "t_pre0": None}
+        to_score = misses + shadow
+        if not to_score:
+            self._respond(ctx, None, fut)
+            return
+        t1 = self.clock()
+        ids, offs, ok = self._tokenize(req.query, to_score, errors)
+        n_shadow = sum(1 for it in ok if it in shadow)
+        ctx["ok"], ctx["shadow"] = ok, n_shadow
+        t2 = self.clock()
+        ctx["t_tok"], ctx["t_pre0"] = t2 - t1, t2
+        if not ok:
+            self._respond(ctx, None, fut)
+            return
+        packed = ingest.pack_flat_native(ids, offs, None, self.max_seq)
+        ctx["flops"] = self._work_flops(packed)
+        if hasattr(self.scorer, "submit_packed"):
+            inner = self.scorer.submit_packed(packed)
+            inner.add_done_callback(lambda f: self._after_model(ctx, f, fut))
+        else:
+            res = self.scorer.score_packed(packed)
+            self._respond(ctx, res, fut)
+
+    def _tokenize(self, query: Query, items: list, errors: list):
+        """Eq-1 prompts of ``items`` -> (flat ids, offsets, items kept), tokenized in one native batch.
+        Segments begin and end with tags, so a prompt's token count is the sum of its segments'
+        counts: a prompt within the budget is exactly what truncate_description would return
+        unchanged, and only over-budget prompts take the per-item truncation path (corpus.py:314-345)."""
+        prompts = [assemble_prompt(query, it).full_prompt() for it in items]
+        ids, offs = ingest.encode_batch_arrays(prompts, self.vocab)
+        lens = np.diff(offs)
+        over = np.nonzero(lens > self.token_budget)[0]
+        if len(over) == 0:
+            return ids, offs, list(items)
+        keep, fixed = [], {}
+        for i in over:
+            try:
+                fixed[int(i)] = truncate_description(assemble_prompt(query, items[i]), self.token_budget,
+                                                     self.vocab).full_prompt()
+            except PromptBudgetError as e:          # per-item rejection (SPEC.md:697)
+                errors.append({"item_id": items[i].id, "error": str(e)})
+                fixed[int(i)] = None
+        for i in range(len(items)):
+            if fixed.get(i, "") is not None:
+                keep.append(i)
+        prompts = [fixed.get(i) or prompts[i] for i in keep]
+        if not prompts:
+            return ids[:0], np.zeros(1, np.int64), []
+        ids, offs = ingest.encode_batch_arrays(prompts, self.vocab)
+        return ids, offs, [items[i] for i in keep]
+
+    def _after_model(self, ctx, f, fut):
+        try:
+            res = f.result()
+        except BaseException as e:
+            fut.set_exception(e)
+            return
+        try:
+            self._respond(ctx, res, fut)
+        except BaseException as e:       # pragma: no cover
+            fut.set_exception(e)
+
+    def _work_flops(self, packed):
+        cfg = self.model_config
+        if cfg is None:
+            return None
+        from .prefixcache import request_flops
+
+        P = int(packed.prefix_lens[0])
+        return (request_flops(cfg, P, packed.suffix_lens, True), request_flops(cfg, P, packed.suffix_lens, False))
+
+    def _respond(self, ctx, res, fut):
+        req, scores = ctx["req"], ctx["scores"]
+        now = self.clock()
+        t_pre = (now - ctx["t_pre0"]) if ctx["t_pre0"] is not None else 0.0
+        with self._lock:
+            if res is not None:
                 self.model_calls += 1
-                self.items_scored += len(ok)
-                now = self.clock()
-                for it, p in zip(ok, res.p_yes):
-                    scores[it.id] = (float(p), "model")
-                    self.cache.insert((self.model_version, qh, it.id), float(p), now)
-            t_pre = self.clock() - t2
+                n_model = len(ctx["ok"]) - ctx["shadow"]
+                self.items_scored += n_model
+                self._item_log.append((now, n_model))
+                fl = ctx.get("flops")
+                if fl is not None:
+                    self._flops_shared += fl[0]
+                    self._flops_indep += fl[1]
+                for it, p in zip(ctx["ok"], res.p_yes):
+                    p = float(p)
+                    if it.id in scores:                       # shadow re-score of a cache hit
+                        diff = abs(p - scores[it.id][0])
+                        self._shadow["checked"] += 1
+                        self._shadow["max_abs_diff"] = max(self._shadow["max_abs_diff"], diff)
+                        self._shadow["violations"] += int(diff > self.shadow_tol)
+                        continue
+                    scores[it.id] = (p, "model")
+                    self.cache.insert((self.model_version, ctx["qh"], it.id), p, now)
         ids = list(scores.keys())
         out = []
         if ids:
             ranked = rank_items([scores[i][0] for i in ids], ids)
             out = [{"item_id": i, "p_yes": p, "source": scores[i][1]} for i, p in zip(ranked.item_ids, ranked.scores)]
         t_end = self.clock()
-        return ScoreResponse(req.request_id, depth, out,
-                             {"queue": 1e3 * (t_admit - arrival) if req.arrival is not None else 1e3 * (t_admit - t0),
-                              "tokenize": 1e3 * t_tok, "prefill": 1e3 * t_pre, "total": 1e3 * (t_end - t0)},
-                             unscored, errors)
+        arrival = ctx["arrival"]
+        total = 1e3 * (t_end - (arrival if req.arrival is not None else ctx["t0"]))
+        resp = ScoreResponse(req.request_id, ctx["depth"], out,
+                             {"queue": 1e3 * (ctx["t_admit"] - (arrival if req.arrival is not None else ctx["t0"])),
+                              "tokenize": 1e3 * ctx["t_tok"], "prefill": 1e3 * t_pre, "total": total},
+                             ctx["unscored"], ctx["errors"])
+        with self._lock:
+            self._lat.append((t_end, total))
+        fut.set_result(resp)
+
+    # ------------------------------------------------------------------ metrics
+    def _prune(self, now):
+        lo = now - self.window_s
+        while self._lat and self._lat[0][0] < lo:
+            self._lat.pop(0)
+        while self._item_log and self._item_log[0][0] < lo:
+            self._item_log.pop(0)
+
+    def p95_ms(self, now: float | None = None):
+        """Nearest-rank p95 of request latency over the sliding window."""
+        now = self.clock() if now is None else now
+        with self._lock:
+            self._prune(now)
+            lat = sorted(x for _, x in self._lat)
+        if not lat:
+            return None
+        return lat[max(1, int(np.ceil(0.95 * len(lat)))) - 1]
 
     def metrics(self) -> dict:
         """GET /v1/metrics shape."""
-        return {"cache": self.cache.stats(),
-                "pid": {"depth": self.pid.depth if self.pid else None},
-                "shaper": self.shaper.stats() if self.shaper else {"deferred": 0, "mean_defer_ms": 0.0},
-                "engine": {"model_calls": self.model_calls, "items_scored": self.items_scored}}
+        now = self.clock()
+        p95 = self.p95_ms(now)
+        with self._lock:
+            items_window = sum(n for _, n in self._item_log)
+            saved = (100.0 * (1.0 - self._flops_shared / self._flops_indep)) if self._flops_indep > 0 else 0.0
+            return {"cache": self.cache.stats(),
+                    "pid": {"depth": self.pid.depth if self.pid else None, "p95_ms": p95},
+                    "shaper": self.shaper.stats() if self.shaper else {"deferred": 0, "mean_defer_ms": 0.0},
+                    "engine": {"items_per_sec": items_window / self.window_s if self._item_log else 0.0,
+                               "flops_saved_pct": saved, "model_calls": self.model_calls,
+                               "items_scored": self.items_scored},
+                    "shadow": dict(self._shadow)}

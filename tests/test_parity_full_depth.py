@@ -1,0 +1,113 @@
+"""Full-depth (28-layer) parity at every BASELINE model config, against the CPU fp32 oracle.
+
+VERDICT r1 "next #1": the benchmarked configs' per-query top-10 ordering and the 28-layer margins.
+Every case runs the BASELINE model at its full depth and width on the device (through the C-ABI)
+and the same bf16-valued weights in the numpy fp32 oracle, on item samples the oracle finishes in
+seconds:
+
+  * C2 (0.6B-shaped) and C4 (1.7B pruned 40%): one 64-token prefix shared by 32 items of the
+    config's item length, in both input families (template: every item ends in <|ans|>; spread:
+    random last token), top-10 gate on;
+  * C3 (1.7B-shaped): 3 items of 1,024 tokens (the full-length descriptions) and 1 of 960 under a
+    64-token prefix, top-3 gate on;
+  * C5-shaped: two ragged requests packed into one launch on the C4 model (10 and 12 items,
+    item lengths drawn from U{64..1024}), top-10 gate on per request.
+
+Gates, all fixed before the run (north_star):
+  * per item |Δp_yes| <= TOL_P = 1e-2;
+  * per request, the device's top-k equals the oracle's under rank_items, except that oracle pairs
+    closer than NEAR_TIE = 5e-3 may swap.  NEAR_TIE is twice the per-item error budget ERR_BUDGET =
+    2.5e-3 (the largest 28-layer |Δp| measured in round 1); it does not depend on this run's own
+    errors, and the near-tie count is printed per case;
+  * |Δlogit| (yes and no logits) is printed, and gated loosely at 0.25 as a sanity bound.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+torch = pytest.importorskip("torch")
+
+import oracle.model as OM  # noqa: E402
+import oracle.prefixcache as OP  # noqa: E402
+import oracle.scoring as OS  # noqa: E402
+from paper_2510_22101_b200 import CONFIGS, SharedBatch, init_device_weights, pack_requests  # noqa: E402
+from paper_2510_22101_b200.engine import PrefillScorer  # noqa: E402
+from tests.synth import make_shared  # noqa: E402
+
+TOL_P = 1e-2
+ERR_BUDGET = 2.5e-3
+NEAR_TIE = 2 * ERR_BUDGET
+TOL_LOGIT = 0.25
+
+_cache = {}
+
+
+def models(name):
+    """(device scorer, oracle weights) for a BASELINE config at full depth; one config resident at a
+    time (C3's oracle weights alone are 5.6 GB of fp32)."""
+    if name not in _cache:
+        _cache.clear()
+        cfg = CONFIGS[name]
+        _cache[name] = (PrefillScorer(init_device_weights(cfg, 0, "cuda")), OM.init_weights(cfg, 0))
+    return _cache[name]
+
+
+def oracle_logits(ow, sb):
+    osb = OP.SharedBatch(list(sb.prefix_tokens), [list(s) for s in sb.suffixes])
+    return np.asarray([[l[1], l[2]] for l in OP.score_shared_batch(ow, osb)], dtype=np.float64)
+
+
+def check(name, batches, k):
+    scorer, ow = models(name)
+    res = scorer.score_packed(pack_requests(batches, scorer.config.max_seq))
+    ref = np.concatenate([oracle_logits(ow, sb) for sb in batches])
+    p_ref = 1.0 / (1.0 + np.exp(-(ref[:, 0] - ref[:, 1])))
+    dp = np.abs(res.p_yes.astype(np.float64) - p_ref)
+    dl = np.abs(res.logits2.astype(np.float64) - ref)
+    ties, off = 0, 0
+    for sb in batches:
+        n = sb.n_items
+        pr, pg = p_ref[off:off + n], res.p_yes[off:off + n]
+        kk = min(k, n)
+        assert OS.topk_equal_modulo_ties(pr, pg, kk, NEAR_TIE), (
+            f"{name}: top-{kk} differs beyond declared near-ties: oracle {OS.rank_items(pr)[:kk]} "
+            f"device {OS.rank_items(pg)[:kk]}")
+        t = OS.near_tie_pairs(pr, kk, NEAR_TIE)
+        if t == 0:
+            assert OS.rank_items(pr)[:kk] == OS.rank_items(pg)[:kk]
+        ties += t
+        off += n
+    print(f"\n{name}: items={len(dp)} max|dp|={dp.max():.2e} mean|dp|={dp.mean():.2e} "
+          f"max|dlogit|={dl.max():.2e} near-ties(<{NEAR_TIE:g})={ties} top-{k} gate on")
+    assert dp.max() <= TOL_P
+    assert dl.max() <= TOL_LOGIT
+    return dp.max()
+
+
+@pytest.mark.parametrize("family", ["template", "spread"])
+@pytest.mark.parametrize("name,S", [("C4", 100), ("C2", 128)])
+def test_full_depth_top10(name, S, family):
+    rng = np.random.default_rng({"C4": 401, "C2": 402}[name] + (family == "spread"))
+    check(name, [make_shared(rng, 64, [S] * 32, family)], 10)
+
+
+def test_c3_full_depth_long_items():
+    rng = np.random.default_rng(403)
+    check("C3", [make_shared(rng, 64, [1024, 1024, 1024, 960], "spread")], 3)
+
+
+def test_c5_shaped_ragged_pack_full_depth():
+    """Two C5-shaped requests (items ~U{10..500} truncated to the oracle's budget: 10 and 12 items;
+    item tokens ~U{64..1024}) in ONE launch on the 28-layer C4 model."""
+    rng = np.random.default_rng(405)
+    batches = [make_shared(rng, 64, [int(x) for x in rng.integers(64, 1025, n)], fam)
+               for n, fam in ((10, "template"), (12, "spread"))]
+    assert all(64 <= len(s) <= 1024 for sb in batches for s in sb.suffixes)
+    check("C4", batches, 10)
+
+
+def test_release_models():
+    _cache.clear()
+    torch.cuda.empty_cache()

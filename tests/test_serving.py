@@ -129,3 +129,123 @@ def test_service_per_item_budget_error():
 
 def test_query_hash_normalizes():
     assert query_hash("Rust  Engineer ") == query_hash("rust engineer") != query_hash("rust engineers")
+
+
+# ----------------------------------------------------------------------------- concurrency model
+class SlowScorer(FakeScorer):
+    """Fake scorer that takes ``delay`` seconds per call (to exercise overlap and the PID loop)."""
+
+    def __init__(self, delay):
+        super().__init__()
+        self.delay = delay
+        self.active = self.max_active = 0
+        import threading
+        self.lock = threading.Lock()
+
+    def score_packed(self, packed):
+        import time
+        with self.lock:
+            self.active += 1
+            self.max_active = max(self.max_active, self.active)
+        time.sleep(self.delay)
+        with self.lock:
+            self.active -= 1
+        return super().score_packed(packed)
+
+
+def test_submit_is_concurrent_and_matches_sync():
+    """requests are processed concurrently up to the worker-pool limit; results equal
+    the synchronous path's."""
+    fs = SlowScorer(0.05)
+    svc = ScoringService(fs, model_version="v1", workers=4)
+    reqs = [ScoreRequest(Query(f"q{i}", f"query {i}"), items(20, seed=i), f"r{i}") for i in range(8)]
+    futs = [svc.submit(r) for r in reqs]
+    got = [f.result(timeout=30) for f in futs]
+    assert fs.max_active > 1 and fs.calls == 8
+    ref = ScoringService(FakeScorer(), model_version="v1")
+    for r, g in zip(reqs, got):
+        want = ref.handle_score_request(r)
+        assert [(s["item_id"], s["p_yes"]) for s in g.scores] == [(s["item_id"], s["p_yes"]) for s in want.scores]
+    svc.close(); ref.close()
+
+
+def test_shaper_defers_without_blocking_the_caller():
+    """A deferred admission waits in the admission queue, not in submit(): submit returns at once
+    and the deferred request still completes, after its admit time."""
+    import time
+
+    svc = ScoringService(FakeScorer(), model_version="v1",
+                         shaper=TokenBucketShaper(rate=5.0, burst=1, max_defer=0.5), workers=2)
+    t0 = time.monotonic()
+    futs = [svc.submit(ScoreRequest(Query("q", "x"), items(3, seed=i), f"r{i}", arrival=t0)) for i in range(3)]
+    assert time.monotonic() - t0 < 0.1                      # no sleep in the caller
+    resp = [f.result(timeout=10) for f in futs]
+    queue = [r.timings_ms["queue"] for r in resp]
+    assert queue[0] < 50 and 150 <= queue[1] and 350 <= queue[2] <= 700     # 1/R = 200 ms, clamp 500 ms
+    assert svc.metrics()["shaper"]["deferred"] == 2
+    svc.close()
+
+
+def test_metrics_loop_drives_the_pid_depth():
+    """The single metrics loop feeds the sliding-window p95 to the PID: with every
+    request slower than the target, depth falls from its initial value."""
+    import time
+
+    svc = ScoringService(SlowScorer(0.03), model_version="v1", pid=PidController(depth=250),
+                         target_p95_ms=10.0, pid_interval=0.05, window_s=5.0, workers=2)
+    for i in range(6):
+        svc.handle_score_request(ScoreRequest(Query(f"q{i}", f"w {i}"), items(5, seed=i), f"r{i}"))
+    time.sleep(0.3)
+    m = svc.metrics()
+    assert m["pid"]["p95_ms"] >= 30 and svc.pid.depth < 250
+    svc.close()
+
+
+def test_metrics_engine_fields():
+    """GET /v1/metrics engine block: items_per_sec over the window and the FLOPs saved
+    by computing each prefix once (W1 accounting)."""
+    from paper_2510_22101_b200 import CONFIGS
+    from paper_2510_22101_b200.prefixcache import request_flops, throughput_gain
+
+    cfg = CONFIGS["TINY"]
+    svc = ScoringService(FakeScorer(), model_version="v1", model_config=cfg, window_s=60.0)
+    r = svc.handle_score_request(ScoreRequest(Query("q", "data engineer"), items(10), "r"))
+    m = svc.metrics()["engine"]
+    assert m["items_scored"] == 10 and m["items_per_sec"] > 0
+    assert 0 < m["flops_saved_pct"] < 100
+    # uniform suffixes: counted-FLOP ratio vs independent passes ~ throughput_gain (SPEC.md:295, 5%)
+    for P, S in ((50, 150), (64, 100), (100, 100)):
+        ratio = request_flops(cfg, P, [S] * 64, False) / request_flops(cfg, P, [S] * 64, True)
+        assert abs(ratio / throughput_gain(P, S) - 1) < 0.05, (P, S, ratio)
+    svc.close()
+
+
+def test_shadow_scoring_checks_hits_within_tolerance():
+    svc = ScoringService(FakeScorer(), model_version="v1", shadow_rate=1.0)
+    req = ScoreRequest(Query("q", "rust"), items(12), "r")
+    svc.handle_score_request(req)
+    r2 = svc.handle_score_request(req)
+    assert all(s["source"] == "cache" for s in r2.scores)
+    sh = svc.metrics()["shadow"]
+    assert sh["checked"] == 12 and sh["violations"] == 0
+    svc.close()
+
+
+def test_batched_tokenize_equals_per_item_truncation():
+    """The service's one-batch tokenization equals the per-item pipeline (assemble -> truncate ->
+    encode, corpus.py:302-345) for items below, at and above the budget, and rejects the same items."""
+    svc = ScoringService(FakeScorer(), model_version="v1", token_budget=60)
+    its = items(40, seed=3)
+    q = Query("q", "rust systems engineer")
+    errors = []
+    ids, offs, ok = svc._tokenize(q, its, errors)
+    want, want_err = [], []
+    for it in its:
+        try:
+            want.append(ingest.encode(truncate_description(assemble_prompt(q, it), 60).full_prompt()))
+        except PromptBudgetError:
+            want_err.append(it.id)
+    assert [e["item_id"] for e in errors] == want_err
+    assert [ids[offs[i]:offs[i + 1]].tolist() for i in range(len(ok))] == want
+    assert any(len(w) == 60 for w in want) and any(len(w) < 60 for w in want)
+    svc.close()
