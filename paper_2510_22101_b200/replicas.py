@@ -82,7 +82,7 @@ class ReplicaWorker(threading.Thread):
             self.stream = torch.cuda.Stream(scorer.device)
         self._jobs: list[_Job] = []
         self._cv = threading.Condition()
-        self._stop = False
+        self._stopping = False
         self.outstanding_tokens = 0
         self.launches = 0
         self.items_scored = 0
@@ -91,7 +91,7 @@ class ReplicaWorker(threading.Thread):
     # ------------------------------------------------------------------ queue
     def enqueue(self, job: _Job) -> None:
         with self._cv:
-            if self._stop:
+            if self._stopping:
                 raise RuntimeError("replica worker stopped")
             self._jobs.append(job)
             self.outstanding_tokens += job.tokens
@@ -99,13 +99,13 @@ class ReplicaWorker(threading.Thread):
 
     def stop(self) -> None:
         with self._cv:
-            self._stop = True
+            self._stopping = True
             self._cv.notify()
 
     def _take(self, block: bool) -> list[_Job]:
         """Smallest pending jobs first, up to the token budget (always at least one job)."""
         with self._cv:
-            while block and not self._jobs and not self._stop:
+            while block and not self._jobs and not self._stopping:
                 self._cv.wait()
             if not self._jobs:
                 return []
@@ -174,7 +174,7 @@ class ReplicaWorker(threading.Thread):
         while True:
             jobs = self._take(block=inflight is None)
             if not jobs and inflight is None:
-                if self._stop:
+                if self._stopping:
                     return
                 continue
             nxt = None

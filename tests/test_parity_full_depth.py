@@ -16,9 +16,9 @@ seconds:
 Gates, all fixed before the run (north_star):
   * per item |Δp_yes| <= TOL_P = 1e-2;
   * per request, the device's top-k equals the oracle's under rank_items, except that oracle pairs
-    closer than NEAR_TIE = 5e-3 may swap.  NEAR_TIE is twice the per-item error budget ERR_BUDGET =
-    2.5e-3 (the largest 28-layer |Δp| measured in round 1); it does not depend on this run's own
-    errors, and the near-tie count is printed per case;
+    closer than NEAR_TIE = 5e-3 (half the per-item tolerance) may swap.  NEAR_TIE is a constant: it
+    does not depend on this run's own errors.  The near-tie count is printed per case; a case
+    without near-ties must match the oracle's top-k exactly;
   * |Δlogit| (yes and no logits) is printed, and gated loosely at 0.25 as a sanity bound.
 """
 
@@ -37,8 +37,7 @@ from paper_2510_22101_b200.engine import PrefillScorer  # noqa: E402
 from tests.synth import make_shared  # noqa: E402
 
 TOL_P = 1e-2
-ERR_BUDGET = 2.5e-3
-NEAR_TIE = 2 * ERR_BUDGET
+NEAR_TIE = 5e-3
 TOL_LOGIT = 0.25
 
 _cache = {}
