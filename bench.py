@@ -270,9 +270,9 @@ def run_ours(args):
     # executed work: the last layer's O-projection + MLP run on the n_items last-token rows only
     flops_exec = flops_step - shape.n_requests * (packed.T // shape.n_requests - shape.n_items) * 2 * (
         cfg.q_width * cfg.d_model + 3 * cfg.d_model * cfg.d_ff)
-    # embed + rope-gather + (L-1) x [QKV, attention, O, gate/up, down] + last layer [QKV, attention,
-    # gather, O, gate/up, down] + head  (RMSNorm is fused into the GEMM epilogues)
-    launches_per_step = 5 * cfg.n_layers + 4
+    # embed + rope-gather + (L-1) x [QKV, attention, O, gate/up, down | QKV, attention, fused tail] + last
+    # layer [QKV, attention, gather, O, gate/up, down] + head  (RMSNorm is fused into the GEMM epilogues)
+    launches = lambda fused: (3 if fused else 5) * (cfg.n_layers - 1) + 6 + 3
 
     def barrier():
         if ws > 1:
@@ -325,7 +325,7 @@ def run_ours(args):
     # (pf_profile_*): per-class time per step, and the dominant kernel's average launch duration
     # under the step's own clocks / power draw (the roofline below).
     lib = _lib.load()
-    n_cls, prof_steps = 7, 10
+    n_cls, prof_steps = 8, 10
     for _ in range(2):                       # back to steady-state power-capped clocks after e2e
         scorer.score_device(dp, check=False)
     _lib.check(lib.pf_profile_enable(1))
@@ -337,34 +337,54 @@ def run_ours(args):
     in_step = {lib.pf_profile_class_name(c).decode(): {"ms_per_step": pms[c] / prof_steps,
                                                        "launches_per_step": pnl[c] // prof_steps}
                for c in range(n_cls)}
-    gu_launch_ms = pms[4] / max(pnl[4], 1)   # PF_PROF_GATE_UP: full-T launches (last layer is class 6)
 
-    # ---------------------------------------------------------------- dominant kernel alone
+    # ---------------------------------------------------------------- dominant kernel
+    # The fused layer tail (O + gate/up + down, one launch per layer, PF_PROF_MLP_FUSED) when it is on;
+    # else the gate/up SwiGLU GEMM (PF_PROF_GATE_UP).  Full-T launches only (the last layer is class 6).
     T, d = packed.T, cfg.d_model
-    A = (torch.randn(T, d, device=dev) * 0.5).to(torch.bfloat16)
-    C = torch.empty(T, cfg.d_ff_pad, device=dev, dtype=torch.bfloat16)
-    B = weights.w_gu[0]
+    fused = pnl[7] > 0
     sp = ctypes.c_void_p(stream.cuda_stream)
-    gemm = lambda: _lib.check(lib.pf_gemm_bf16(A.data_ptr(), d, B.data_ptr(), d, C.data_ptr(), cfg.d_ff_pad,
-                                               T, 2 * cfg.d_ff_pad, d, _lib.EPI_SWIGLU, None, None, None, 0, sp))
+    if fused:
+        k_name = "mlp_fused_kernel (O + gate/up SwiGLU + down, one launch per layer)"
+        k_flops = 2.0 * T * (cfg.q_width * d + 3 * d * cfg.d_ff)
+        dom_launch_ms = pms[7] / pnl[7]
+        attn_in = (torch.randn(T, cfg.q_width, device=dev) * 0.5).to(torch.bfloat16)
+        xb = (torch.randn(T, d, device=dev)).to(torch.bfloat16)
+        rlo = torch.full((T, d), 128, dtype=torch.uint8, device=dev)
+        hb = torch.empty(T, cfg.d_ff_pad, device=dev, dtype=torch.bfloat16)
+        parts = (d + 255) // 256
+        ss_m = torch.empty(parts, T, device=dev)
+        ss_a = torch.empty(parts, T, device=dev)
+        ctr = torch.empty(8 * ((T + 255) // 256) + 64, dtype=torch.uint8, device=dev)
+        kern = lambda: _lib.check(lib.pf_layer_tail(scorer.handle, 0, attn_in.data_ptr(), xb.data_ptr(), rlo.data_ptr(),
+                                                    hb.data_ptr(), ss_m.data_ptr(), ss_a.data_ptr(), T, ctr.data_ptr(),
+                                                    ctr.numel(), sp))
+    else:
+        k_name = "gemm_bf16_kernel<EPI_SWIGLU> (gate/up)"
+        k_flops = 2.0 * T * d * 2 * cfg.d_ff
+        dom_launch_ms = pms[4] / max(pnl[4], 1)
+        A = (torch.randn(T, d, device=dev) * 0.5).to(torch.bfloat16)
+        C = torch.empty(T, cfg.d_ff_pad, device=dev, dtype=torch.bfloat16)
+        B = weights.w_gu[0]
+        kern = lambda: _lib.check(lib.pf_gemm_bf16(A.data_ptr(), d, B.data_ptr(), d, C.data_ptr(), cfg.d_ff_pad,
+                                                   T, 2 * cfg.d_ff_pad, d, _lib.EPI_SWIGLU, None, None, None, 0, sp))
     for _ in range(3):
-        gemm()
+        kern()
     reps = 20
     torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(reps):
-        gemm()
+        kern()
     ev1.record(stream)
     torch.cuda.synchronize()
     k_ms = ev0.elapsed_time(ev1) / reps
-    k_flops = 2.0 * T * d * 2 * cfg.d_ff
-    achieved = k_flops / (gu_launch_ms * 1e-3) / 1e12
+    achieved = k_flops / (dom_launch_ms * 1e-3) / 1e12
     achieved_alone = k_flops / (k_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(args.config, {}).get("gate_up_gemm_dram_bytes")
+            traffic = json.load(f).get(args.config, {}).get("mlp_fused_dram_bytes" if fused else "gate_up_gemm_dram_bytes")
 
     if rank != 0:
         if ws > 1:
@@ -393,13 +413,13 @@ def run_ours(args):
                              "peak_kind": peak_kind},
         "e2e": {"value": e2e_val, "unit": "items/s", "h2d_bytes_per_step": pp.h2d_bytes(),
                 "d2h_bytes_per_step": pp.d2h_bytes(), "ms_per_step": e2e_s / args.steps * 1e3},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches(fused) * args.steps,
         "graph_replay": not args.no_graph,
         # timed inside a long step: the sustained peak is the denominator (B200_PROFILING.md)
-        "roofline": {"kernel": "gemm_bf16_kernel<EPI_SWIGLU> (gate/up)", "bound": "tensor",
+        "roofline": {"kernel": k_name, "bound": "tensor",
                      "achieved": achieved, "peak": peak_sust, "unit": "TFLOP/s",
                      "frac": achieved / peak_sust, "traffic": traffic,
-                     "flops_per_launch": k_flops, "ms_per_launch": gu_launch_ms,
+                     "flops_per_launch": k_flops, "ms_per_launch": dom_launch_ms,
                      "timing": f"CUDA events around each of its launches inside {prof_steps} eager steps",
                      "note": ("peak = MEASURED_PEAKS bf16_tflops_sustained (cuBLAS 8192^3 back to back under the "
                               "same 1 kW cap); frac can exceed 1 when this kernel spends less energy per flop "
@@ -487,7 +507,7 @@ def run_load(args):
     n_dev = min(args.gpus, torch.cuda.device_count())
     scorers = [PrefillScorer(init_device_weights(cfg, 0, f"cuda:{i}"), device=f"cuda:{i}") for i in range(n_dev)]
     pool = ReplicaPool(scorers, token_budget=args.load_token_budget,
-                       max_shard_items=args.c5_shard_items if args.c5_shard_items > 0 else None)
+                       shard_tokens=args.c5_shard_tokens, policy=args.c5_policy)
     svc = ScoringService(pool, model_version="c4-seed0", cache=ScoreCache(), workers=args.c5_workers,
                          model_config=cfg)
     wl = C5Workload(args.seed, args.load_pool)
@@ -568,7 +588,8 @@ def run_load(args):
         "config": {"workload": "C5 mixed load on the C4 model (1.7B-shaped, pruned 40%) through ScoringService",
                    "mean_items_per_request": items_per_req, "mean_tokens_per_request": tok_per_req,
                    "replicas": n_dev, "token_budget_per_launch": args.load_token_budget,
-                   "shard_items": args.c5_shard_items, "handler_workers": args.c5_workers,
+                   "shard_tokens": args.c5_shard_tokens, "policy": args.c5_policy,
+                   "handler_workers": args.c5_workers,
                    "latency": "arrival -> ScoreResponse (Eq-1 assembly, tokenize, pack, H2D, forward, D2H, rank)",
                    "value": "closed-loop capacity, items/s over all replicas"},
         "capacity_items_per_s": capacity, "load_runs": runs, "clocks": clk,
@@ -589,7 +610,8 @@ def main():
     ap.add_argument("--load-seconds", type=float, default=20.0)
     ap.add_argument("--load-requests", type=int, default=300, help="C5: measured requests per load point (min)")
     ap.add_argument("--load-warmup-s", type=float, default=5.0, help="C5: discarded seconds per load point")
-    ap.add_argument("--c5-shard-items", type=int, default=0, help="C5: item-split requests above this many items")
+    ap.add_argument("--c5-shard-tokens", type=int, default=65536, help="C5: max tokens per request shard")
+    ap.add_argument("--c5-policy", default="fifo", choices=["fifo", "sjf"], help="C5: replica queue order")
     ap.add_argument("--c5-workers", type=int, default=8, help="C5: service handler threads")
     ap.add_argument("--load-fracs", type=float, nargs="+", default=[0.5, 0.8])
     ap.add_argument("--load-token-budget", type=int, default=262144)

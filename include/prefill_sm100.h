@@ -192,6 +192,16 @@ PF_API int pf_pack_requests(const int32_t* ids, const int64_t* list_offsets, con
                             int32_t* out_segs, int32_t* out_last, int32_t* out_prefix_lens,
                             int64_t* out_T, int64_t* out_n_seg);
 
+/* The fused layer tail of layer `layer` (mlp.cu) on caller buffers: residual (xb bf16 hi, rlo uint8 lo,
+ * [T x d_model], updated in place) += attn[T x H*dh] . W_o^T, writing the MLP RMSNorm partials ss_mlp
+ * ([d_model/256][T] fp32); hbuf[T x d_ff_pad] = SwiGLU of the normalised residual; residual += hbuf .
+ * W_down^T, writing ss_attn.  The same arithmetic as EPI_RESID_ADD_NORM -> EPI_SWIGLU (row_ss =
+ * ss_mlp) -> EPI_RESID_ADD_NORM through pf_gemm_bf16_ex, in one launch.  counters: device scratch of
+ * >= 8 * ceil(T / 256) bytes (zeroed by the call). */
+PF_API int pf_layer_tail(pf_model* model, int layer, const void* attn, void* xb, void* rlo, void* hbuf,
+                         float* ss_mlp, float* ss_attn, int T, void* counters, size_t counter_bytes,
+                         pf_stream_t stream);
+
 /* In-step kernel timing (measurement only).  pf_profile_enable(1) makes every eager pf_score /
  * pf_score_host / pf_score_capture call bracket each launch with CUDA events on its stream, tagged
  * by kernel class (PF_PROF_*); launches recorded while the stream is capturing a graph are skipped.
@@ -207,7 +217,8 @@ enum {
   PF_PROF_GATE_UP = 4,     /* gate/up GEMM + SwiGLU epilogue */
   PF_PROF_DOWN = 5,        /* down GEMM + residual + RMSNorm statistic */
   PF_PROF_LAST_LAYER = 6,  /* last layer's row gather + O/gate-up/down on the n_items last rows */
-  PF_PROF_CLASSES = 7
+  PF_PROF_MLP_FUSED = 7,   /* fused O + gate/up + down layer tail (one launch per layer, mlp.cu) */
+  PF_PROF_CLASSES = 8
 };
 PF_API int pf_profile_enable(int on);
 PF_API int pf_profile_read(double* ms, int* launches, int n_classes);
@@ -216,6 +227,9 @@ PF_API const char* pf_profile_class_name(int cls);
 /* Debug hook: CTA 0 of the attention kernel appends {event, role, unit, block, globaltimer}
  * records (uint64) to device_buf (NULL disables).  Used by tools/attn_trace.py. */
 PF_API int pf_debug_set_trace(void* device_buf, unsigned int capacity);
+/* Debug: the fused layer tail accumulates ns / counts per wait site into device_buf (u64[16]); null
+ * disables. */
+PF_API int pf_debug_set_mlp_stats(void* device_buf);
 
 PF_API const char* pf_last_error(void);
 PF_API const char* pf_version(void);

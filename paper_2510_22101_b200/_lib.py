@@ -22,7 +22,7 @@ EPI_BF16, EPI_ROPE_BF16, EPI_SWIGLU, EPI_RESID_ADD, EPI_RESID_ADD_NORM = 0, 1, 2
 # Every symbol include/prefill_sm100.h declares (tests check the .so exports all of them).
 EXPORTED_SYMBOLS = (
     "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host", "pf_score_capture",
-    "pf_validate_packed",
+    "pf_validate_packed", "pf_layer_tail", "pf_debug_set_mlp_stats",
     "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
     "pf_last_error", "pf_version", "pf_debug_set_trace", "pf_profile_enable", "pf_profile_read", "pf_profile_class_name",
     "pf_tokenize", "pf_tokenize_spans", "pf_tokenize_batch", "pf_pack_sizes", "pf_pack_requests",
@@ -91,6 +91,8 @@ _SIGS = {
     "pf_score": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "pf_score_capture": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P,
                               ctypes.POINTER(PfCapture), _P]),
+    "pf_debug_set_mlp_stats": (_I, [_P]),
+    "pf_layer_tail": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _I, _P, ctypes.c_size_t, _P]),
     "pf_validate_packed": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, _P]),
     "pf_score_host": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _I, _I, _P, ctypes.c_size_t, _P, _P, _P]),
     "pf_gemm_bf16": (_I, [_P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),

@@ -152,6 +152,8 @@ struct Workspace {
   float *logits2, *p_yes;
   int* bad;
   int* verr;         // pf_score under PF_VALIDATE=1: device bounds-check result (launch_validate_packed)
+  uint32_t* mlp_ctr; // [n_layers][mlp_counter_words(T)] row-block completion counters of the fused tail
+  size_t mlp_ctr_bytes;
   size_t total;
 };
 
@@ -180,6 +182,8 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   w.p_yes = reinterpret_cast<float*>(take((size_t)n_items * 4));
   w.bad = reinterpret_cast<int*>(take(16));
   w.verr = reinterpret_cast<int*>(take(16));
+  w.mlp_ctr_bytes = (size_t)d.n_layers * mlp_counter_words(T) * 4;
+  w.mlp_ctr = reinterpret_cast<uint32_t*>(take(w.mlp_ctr_bytes));
   w.total = off;
   return w;
 }
@@ -189,6 +193,9 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
 extern "C" {
 
 const char* pf_last_error(void) { return g_err; }
+int pf_debug_set_mlp_stats(void* device_buf) {
+  return debug_set_mlp_stats(reinterpret_cast<unsigned long long*>(device_buf));
+}
 int pf_debug_set_trace(void* device_buf, unsigned int capacity) {
   return debug_set_attention_trace(reinterpret_cast<unsigned long long*>(device_buf), capacity);
 }
@@ -287,8 +294,8 @@ struct ProfScope {
     if (idx >= 0) cudaEventRecord(g_prof.ev[2 * idx + 1], st);
   }
 };
-const char* const kProfNames[PF_PROF_CLASSES] = {"elementwise", "qkv_rope", "attention", "o_proj",
-                                                 "gate_up",     "down",     "last_layer"};
+const char* const kProfNames[PF_PROF_CLASSES] = {"elementwise", "qkv_rope", "attention",  "o_proj",
+                                                 "gate_up",     "down",     "last_layer", "mlp_fused"};
 }  // namespace
 
 #define PF_PROF(c) ProfScope _pf_prof_scope_##__LINE__(c, st)
@@ -300,6 +307,18 @@ static int mrev_enabled() {
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v;
+}
+
+// PF_MLP_FUSED=1: the layer tail as mlp.cu's one persistent launch instead of three GEMM launches
+// (O, gate/up, down).  Off by default: bit-identical, but measured 7-20% slower per layer than the
+// three specialised kernels.
+static bool mlp_fused_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PF_MLP_FUSED");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1 && gemm_cta_group() == 2;
 }
 
 static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, const int32_t* segs,
@@ -315,6 +334,11 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
   // rsqrt(ss/d + eps): no atomics, so a pass is bit-reproducible (norm gains are folded into
   // w_qkv / w_gu by the caller, include/prefill_sm100.h).
   int rc;
+  const bool fused = mlp_fused_enabled() && cap == nullptr;
+  if (fused) {
+    cudaError_t e = cudaMemsetAsync(w.mlp_ctr, 0, w.mlp_ctr_bytes, st);
+    if (e != cudaSuccess) return fail(-4, "counter memset: %s", cudaGetErrorString(e));
+  }
   {
     PF_PROF(PF_PROF_ELEMENTWISE);
     if ((rc = launch_embed(ids, d.embedding, nullptr, w.xb, w.rlo, w.ss_attn, T, d.d_model, st))) return rc;
@@ -364,6 +388,16 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
       if ((rc = launch_gemm(dn, &m->tm_down[l], st))) return rc;
       return launch_head(nullptr, w.hi_c, w.lo_c, nullptr, n_items, d.d_model, d.ln_final, d.w_yes, d.w_no,
                          eps, logits2, p_yes, bad, st);
+    }
+    if (fused) {
+      MlpDesc md{};
+      md.attn = w.attn; md.xb = w.xb; md.rlo = w.rlo; md.hbuf = w.hbuf;
+      md.M = T; md.d = d.d_model; md.kq = m->attn_k; md.fp = d.d_ff_pad;
+      md.counters = w.mlp_ctr + (size_t)l * mlp_counter_words(T);
+      md.ss_mlp = w.ss_mlp; md.ss_attn = w.ss_attn; md.ss_ld = T; md.inv_d = inv_d; md.eps = eps;
+      PF_PROF(PF_PROF_MLP_FUSED);
+      if ((rc = launch_mlp_fused(md, &m->tm_o[l], &m->tm_gu[l], &m->tm_down[l], st))) return rc;
+      continue;
     }
     GemmDesc o{};
     o.A = w.attn; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
@@ -578,6 +612,25 @@ int pf_gemm_bf16_ex(const pf_gemm_args* a, pf_stream_t stream) {
   g.inv_d = a->inv_d; g.eps = a->eps;
   g.rope_cs = a->rope_cs;
   return launch_gemm(g, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_layer_tail(pf_model* m, int layer, const void* attn, void* xb, void* rlo, void* hbuf, float* ss_mlp,
+                  float* ss_attn, int T, void* counters, size_t counter_bytes, pf_stream_t stream) {
+  if (!m) return fail(-1, "null model handle");
+  if (layer < 0 || layer >= m->d.n_layers || T < 1) return fail(-1, "pf_layer_tail: layer %d / T %d", layer, T);
+  if (!attn || !xb || !rlo || !hbuf || !ss_mlp || !ss_attn || !counters) return fail(-1, "pf_layer_tail: null buffer");
+  const size_t need = mlp_counter_words(T) * 4;
+  if (counter_bytes < need) return fail(-5, "pf_layer_tail: counters need %zu bytes", need);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(counters, 0, need, st);
+  if (e != cudaSuccess) return fail(-4, "pf_layer_tail memset: %s", cudaGetErrorString(e));
+  MlpDesc md{};
+  md.attn = attn; md.xb = xb; md.rlo = rlo; md.hbuf = hbuf;
+  md.M = T; md.d = m->d.d_model; md.kq = m->attn_k; md.fp = m->d.d_ff_pad;
+  md.counters = static_cast<uint32_t*>(counters);
+  md.ss_mlp = ss_mlp; md.ss_attn = ss_attn; md.ss_ld = T;
+  md.inv_d = 1.0f / (float)m->d.d_model; md.eps = m->d.rms_eps;
+  return launch_mlp_fused(md, &m->tm_o[layer], &m->tm_gu[layer], &m->tm_down[layer], st);
 }
 
 int pf_rmsnorm(const float* x, const float* gamma, void* y, int T, int d, float eps, pf_stream_t stream) {

@@ -49,6 +49,10 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 #ifndef PF_ROPE_EPI_WARPS
 #define PF_ROPE_EPI_WARPS 4
 #endif
+// Mainloop stages of the plain / SwiGLU epilogues at CG = 2 (A/B builds: -DPF_PLAIN_STAGES=5)
+#ifndef PF_PLAIN_STAGES
+#define PF_PLAIN_STAGES 6
+#endif
 // Internal variant of EPI_RESID_ADD_NORM for short K (the C4 O projection, K = 1280): 4 mainloop stages
 // and a 4-deep ring, so a tile's whole residual (4 chunks) is requested while its MMAs run.  At K >= 2048
 // the fifth mainloop stage is worth more (tools/gemm_bench.py: C4 O 127.5 -> 123.4 us, C2 O 113 -> 116).
@@ -68,7 +72,7 @@ struct GemmCfg {
   static constexpr int RBD = DEEP ? 4 : PF_RB_DEPTH;         // ring depth (chunks in flight per warp)
   static constexpr bool ROPE = EPI == EPI_ROPE_BF16;
   // the RoPE epilogue stages a whole 256-column tile (4 boxes per warp) and gives up a stage for it
-  static constexpr int STAGES = DEEP ? 4 : RING ? PF_RING_STAGES : ROPE ? (CG == 2 ? 5 : 3) : (CG == 2 ? 6 : 4);
+  static constexpr int STAGES = DEEP ? 4 : RING ? PF_RING_STAGES : ROPE ? (CG == 2 ? 5 : 3) : (CG == 2 ? PF_PLAIN_STAGES : 4);
   // ring: RBD (hi, lo) chunk slots per epilogue warp; otherwise 2 (RoPE: 4) staging boxes per warp
   static constexpr int EPI_BYTES = RING ? 4 * RBD * RB_SLOT : 4 * (ROPE ? 4 : 2) * GEMM_STG_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;

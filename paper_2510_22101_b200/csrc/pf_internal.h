@@ -104,6 +104,26 @@ int launch_validate_packed(const int32_t* ids, const int32_t* pos, const int32_t
                            const int32_t* work, int n_work, const int32_t* last_idx, int n_items, int T, int vocab,
                            int max_seq, int* err, cudaStream_t stream);
 
+// Fused post-attention layer tail (mlp.cu): O projection + residual, gate/up + SwiGLU, down +
+// residual in one persistent launch with per-row-block completion counters.
+struct MlpDesc {
+  const void* attn;     // [M x kq] bf16 attention output
+  void* xb;             // [M x d] bf16 residual hi (updated in place)
+  void* rlo;            // [M x d] uint8 residual lo (updated in place)
+  void* hbuf;           // [M x fp] bf16 SwiGLU output
+  int M, d, kq, fp;
+  uint32_t* counters;   // mlp_counter_words(M) zeroed words
+  float* ss_mlp;        // [d/256][ss_ld] written by O, read by gate/up
+  float* ss_attn;       // [d/256][ss_ld] written by down (next layer's QKV reads it)
+  int ss_ld;
+  float inv_d, eps;
+};
+int launch_mlp_fused(const MlpDesc& d, const CUtensorMap* b_o, const CUtensorMap* b_gu, const CUtensorMap* b_dn,
+                     cudaStream_t stream);
+size_t mlp_counter_words(int M);
+// debug: ns / counts per wait site of the fused tail, summed over CTAs (null disables)
+int debug_set_mlp_stats(unsigned long long* buf);
+
 struct AttnDesc {
   const void* qkv;        // [T x (H+2Hkv)*dh] bf16 (RoPE already applied to q, k)
   void* out;              // [T x H*dh] bf16

@@ -13,9 +13,13 @@ forwards of every device.
   different replicas (each shard recomputes the short prefix); the future resolves
   when every shard is back, with scores in the request's item order.
 * Dispatch: the replica with the fewest outstanding tokens (ties: lowest index).
-* Each worker coalesces everything queued on it, up to ``token_budget`` tokens, into one
-  ``pf_score`` launch (``concat_packed``), smallest pending jobs first, and keeps up to two
-  launches in flight: while the device runs launch k, the thread joins and enqueues launch k+1
+* Sharding (``submit_token_arrays``): a request is item-split into shards of at most
+  ``shard_tokens`` tokens, and into at least one shard per replica when it has enough items, so a
+  large request runs on every replica at once and no launch grows past the budget; shards complete
+  into one future in item order.
+* Each worker coalesces queued jobs, up to ``token_budget`` tokens, into one ``pf_score`` launch
+  (``concat_packed``), oldest first (``policy="fifo"``; "sjf" = smallest first), and keeps up to
+  two launches in flight: while the device runs launch k, the thread joins and enqueues launch k+1
   (H2D from pinned memory on the same stream), then waits for k and hands its scores out.
 """
 
@@ -72,12 +76,15 @@ class _Shards:
 class ReplicaWorker(threading.Thread):
     """Serves one PrefillScorer: a queue of packed jobs -> batched, pipelined pf_score launches."""
 
-    def __init__(self, scorer, token_budget: int = 1 << 18, name: str | None = None):
+    def __init__(self, scorer, token_budget: int = 1 << 18, name: str | None = None, policy: str = "fifo"):
         import torch
 
         super().__init__(name=name or f"replica-{scorer.device}", daemon=True)
+        if policy not in ("fifo", "sjf"):
+            raise ValueError("policy must be 'fifo' or 'sjf'")
         self.scorer = scorer
         self.token_budget = int(token_budget)
+        self.policy = policy
         with torch.cuda.device(scorer.device):
             self.stream = torch.cuda.Stream(scorer.device)
         self._jobs: list[_Job] = []
@@ -103,13 +110,17 @@ class ReplicaWorker(threading.Thread):
             self._cv.notify()
 
     def _take(self, block: bool) -> list[_Job]:
-        """Smallest pending jobs first, up to the token budget (always at least one job)."""
+        """Pending jobs in policy order (oldest or smallest first), up to the token budget (always
+        at least one job)."""
         with self._cv:
             while block and not self._jobs and not self._stopping:
                 self._cv.wait()
             if not self._jobs:
                 return []
-            self._jobs.sort(key=lambda j: (j.tokens, j.seq))
+            if self.policy == "sjf":
+                self._jobs.sort(key=lambda j: (j.tokens, j.seq))
+            else:
+                self._jobs.sort(key=lambda j: j.seq)
             batch, toks = [], 0
             while self._jobs and (not batch or toks + self._jobs[0].tokens <= self.token_budget):
                 j = self._jobs.pop(0)
@@ -200,10 +211,12 @@ class ReplicaPool:
     """Request-sharded scoring over local GPU replicas: no collective, one host
     thread per replica, scores gathered host-side in request order."""
 
-    def __init__(self, scorers: Sequence, token_budget: int = 1 << 18, max_shard_items: int | None = None):
+    def __init__(self, scorers: Sequence, token_budget: int = 1 << 18, max_shard_items: int | None = None,
+                 shard_tokens: int = 1 << 16, min_shard_items: int = 8, policy: str = "fifo"):
         if not scorers:
             raise ValueError("ReplicaPool: need >= 1 scorer")
-        self.workers = [ReplicaWorker(s, token_budget) for s in scorers]
+        self.workers = [ReplicaWorker(s, token_budget, policy=policy) for s in scorers]
+        self.shard_tokens, self.min_shard_items = int(shard_tokens), int(min_shard_items)
         self.max_seq = scorers[0].config.max_seq
         self.config = scorers[0].config
         # default: split so a request can spread over every replica once it is larger than ~1 launch
@@ -248,6 +261,35 @@ class ReplicaPool:
 
     def submit_packed(self, packed: PackedBatch) -> Future:
         return self._enqueue(packed)
+
+    def shard_bounds(self, item_tokens: np.ndarray) -> list[tuple[int, int]]:
+        """Item ranges of the shards of one request (see the module docstring)."""
+        n = len(item_tokens)
+        total = int(np.sum(item_tokens))
+        k = max(1, -(-total // self.shard_tokens))
+        k = max(k, min(len(self.workers), n // max(1, self.min_shard_items)))
+        k = min(k, n)
+        if k == 1:
+            return [(0, n)]
+        # cut at equal token quantiles (balanced shard cost)
+        cum = np.cumsum(item_tokens)
+        cuts = np.searchsorted(cum, total * np.arange(1, k) / k, side="left") + 1
+        b = [0] + sorted(set(int(c) for c in cuts if 0 < c < n)) + [n]
+        return list(zip(b[:-1], b[1:]))
+
+    def submit_token_arrays(self, ids: np.ndarray, offsets: np.ndarray) -> Future:
+        """One request given as its items' full prompts (flat token ids + offsets, what
+        ingest.encode_batch_arrays returns): sharded, packed natively (LCP split per shard) and
+        scored; the future holds the request's ScoredBatch in item order."""
+        from . import ingest
+
+        offsets = np.asarray(offsets, dtype=np.int64)
+        bounds = self.shard_bounds(np.diff(offsets))
+        shards = []
+        for a, b in bounds:
+            sub = offsets[a:b + 1] - offsets[a]
+            shards.append(ingest.pack_flat_native(ids[offsets[a]:offsets[b]], sub, None, self.max_seq))
+        return self.submit_shards(shards)
 
     def submit_shards(self, shards: Sequence[PackedBatch]) -> Future:
         fut: Future = Future()

@@ -427,12 +427,13 @@ class ScoringService:
         if not ok:
             self._respond(ctx, None, fut)
             return
-        packed = ingest.pack_flat_native(ids, offs, None, self.max_seq)
-        ctx["flops"] = self._work_flops(packed)
-        if hasattr(self.scorer, "submit_packed"):
-            inner = self.scorer.submit_packed(packed)
+        if hasattr(self.scorer, "submit_token_arrays"):      # ReplicaPool: sharded, asynchronous
+            ctx["flops"] = self._work_flops_arrays(ids, offs)
+            inner = self.scorer.submit_token_arrays(ids, offs)
             inner.add_done_callback(lambda f: self._after_model(ctx, f, fut))
         else:
+            packed = ingest.pack_flat_native(ids, offs, None, self.max_seq)
+            ctx["flops"] = self._work_flops(packed)
             res = self.scorer.score_packed(packed)
             self._respond(ctx, res, fut)
 
@@ -483,6 +484,26 @@ class ScoringService:
 
         P = int(packed.prefix_lens[0])
         return (request_flops(cfg, P, packed.suffix_lens, True), request_flops(cfg, P, packed.suffix_lens, False))
+
+    def _work_flops_arrays(self, ids, offs):
+        """(shared, independent) FLOPs of one request from its flat prompt tokens: the LCP of the
+        prompts is the shared prefix (split_shared_prefix rule)."""
+        cfg = self.model_config
+        if cfg is None:
+            return None
+        from .prefixcache import request_flops
+
+        lens = np.diff(offs)
+        first = ids[offs[0]:offs[1]]
+        P = len(first)
+        for i in range(1, len(lens)):
+            row = ids[offs[i]:offs[i + 1]]
+            n = min(P, len(row))
+            neq = np.nonzero(first[:n] != row[:n])[0]
+            P = int(neq[0]) if len(neq) else n
+        if (lens == P).any():
+            P -= 1
+        return (request_flops(cfg, P, lens - P, True), request_flops(cfg, P, lens - P, False))
 
     def _respond(self, ctx, res, fut):
         req, scores = ctx["req"], ctx["scores"]

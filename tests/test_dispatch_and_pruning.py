@@ -150,3 +150,24 @@ def test_prune_kv_groups_keeps_gqa_invariant():
     np.testing.assert_array_equal(pw.layers[0].W_k, w.layers[0].W_k[:, : 5 * 128])
     c4 = apply_recipe(w, PruneRecipe(mlp_sparsity=0.4, kv_groups_to_keep=5))
     assert c4.config.d_ff == 3686 and c4.config.n_heads == 10                # config C4 widths
+
+
+def test_shard_bounds_balance_tokens_and_cover_items():
+    """ReplicaPool.shard_bounds: contiguous item ranges covering the request, at most shard_tokens
+    tokens per shard (unless one item alone exceeds it), at least one shard per replica when the
+    request has min_shard_items items per replica."""
+    from paper_2510_22101_b200.replicas import ReplicaPool
+
+    pool = ReplicaPool.__new__(ReplicaPool)
+    pool.workers = [None] * 4
+    pool.shard_tokens, pool.min_shard_items = 1000, 8
+    rng = np.random.default_rng(0)
+    for n in (1, 5, 31, 32, 200):
+        toks = rng.integers(64, 400, n)
+        b = pool.shard_bounds(toks)
+        assert b[0][0] == 0 and b[-1][1] == n and all(x[1] == y[0] for x, y in zip(b, b[1:]))
+        assert all(hi > lo for lo, hi in b)
+        if n >= 32:
+            assert len(b) >= 4
+        sums = [int(toks[lo:hi].sum()) for lo, hi in b]
+        assert max(sums) <= 1000 + int(toks.max())

@@ -349,3 +349,51 @@ def test_prefix_attention_rescales_and_masked_blocks(lib):
     ref = attention_ref(qkv, packed, H, Hkv, dh)
     assert torch.isfinite(out.float()).all()
     torch.testing.assert_close(out.float(), ref, rtol=2e-2, atol=3e-2)
+
+
+@pytest.mark.parametrize("name,M", [("C4", 3000), ("C2", 1000), ("TINY_GQA", 700), ("C4", 255)])
+def test_layer_tail_fused_equals_three_gemms(lib, name, M):
+    """pf_layer_tail (mlp.cu: O + gate/up SwiGLU + down in one persistent launch with per-row-block
+    completion counters) against the same three epilogues launched one after another through
+    pf_gemm_bf16_ex: bit-identical residual (hi, lo), h and RMSNorm partials."""
+    from paper_2510_22101_b200 import CONFIGS, init_device_weights
+    from paper_2510_22101_b200.engine import PrefillScorer
+
+    cfg = CONFIGS[name].with_(n_layers=1)
+    sc = PrefillScorer(init_device_weights(cfg, 0, "cuda"))
+    w = sc.weights
+    d, kq, fp = cfg.d_model, cfg.q_width, cfg.d_ff_pad
+    attn = rand_bf16(M, kq, scale=0.5, seed=40)
+    x0 = torch.randn(M, d, device="cuda") * 2
+    hi0, lo0 = resid_encode(x0)
+    parts = (d + 255) // 256
+
+    def run(fused):
+        hi, lo = hi0.clone(), lo0.clone()
+        h = torch.zeros(M, fp, device="cuda", dtype=torch.bfloat16)
+        ss_m = torch.zeros(parts, M, device="cuda")
+        ss_a = torch.zeros(parts, M, device="cuda")
+        if fused:
+            ctr = torch.empty(8 * ((M + 255) // 256), dtype=torch.uint8, device="cuda")
+            _lib.check(lib.pf_layer_tail(sc.handle, 0, P(attn), P(hi), P(lo), P(h), P(ss_m), P(ss_a), M,
+                                         P(ctr), ctr.numel(), stream()))
+            torch.cuda.synchronize()
+        else:
+            gemm_ex(lib, A=attn, lda=kq, B=w.w_o[0], ldb=kq, C=lo, ldc=d, M=M, N=d, K=kq,
+                    epilogue=_lib.EPI_RESID_ADD_NORM, xb=hi, ldxb=d, ss_out=ss_m, ss_ld=M)
+            gemm_ex(lib, A=hi, lda=d, B=w.w_gu[0], ldb=d, C=h, ldc=fp, M=M, N=2 * fp, K=d,
+                    epilogue=_lib.EPI_SWIGLU, row_ss=ss_m, ss_ld=M, inv_d=1.0 / d, eps=cfg.rms_eps)
+            gemm_ex(lib, A=h, lda=fp, B=w.w_down[0], ldb=fp, C=lo, ldc=d, M=M, N=d, K=fp,
+                    epilogue=_lib.EPI_RESID_ADD_NORM, xb=hi, ldxb=d, ss_out=ss_a, ss_ld=M)
+        return hi, lo, h, ss_m, ss_a
+
+    ref = run(False)
+    for _ in range(2):                      # twice: counters are re-zeroed per call
+        got = run(True)
+        for a, b in zip(got, ref):
+            assert torch.equal(a, b)
+    # and against fp32 math (one layer tail on the decoded residual)
+    x = resid_decode(hi0, lo0)
+    x1 = x + attn.float() @ w.w_o[0].float().t()
+    assert float((resid_decode(*ref[:2]) - x).abs().max()) > 0        # the tail did change x
+    torch.testing.assert_close(ref[3].sum(0), x1.pow(2).sum(-1), rtol=1e-3, atol=1e-1)

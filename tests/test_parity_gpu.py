@@ -242,16 +242,21 @@ def test_in_step_kernel_profiler():
     run()
     for _ in range(2):
         scorer.score_device(dp, check=False)
-    ms, nl = (ctypes.c_double * 7)(), (ctypes.c_int * 7)()
-    _lib.check(lib.pf_profile_read(ms, nl, 7))
+    ms, nl = (ctypes.c_double * 8)(), (ctypes.c_int * 8)()
+    _lib.check(lib.pf_profile_read(ms, nl, 8))
     _lib.check(lib.pf_profile_enable(0))
     L = cfg.n_layers
-    names = [lib.pf_profile_class_name(c).decode() for c in range(7)]
-    assert names == ["elementwise", "qkv_rope", "attention", "o_proj", "gate_up", "down", "last_layer"]
+    names = [lib.pf_profile_class_name(c).decode() for c in range(8)]
+    assert names == ["elementwise", "qkv_rope", "attention", "o_proj", "gate_up", "down", "last_layer", "mlp_fused"]
     P = 3                                # eager passes: graph_runner's warm-up + 2
-    # per pass: embed/rope-gather scope (the head runs inside the compacted last layer's scope)
-    assert list(nl) == [P, P * L, P * L, P * (L - 1), P * (L - 1), P * (L - 1), P]
-    assert all(ms[c] > 0 for c in range(7))
+    # per pass: embed/rope-gather scope (the head runs inside the compacted last layer's scope); with
+    # PF_MLP_FUSED=1 the first L-1 layers' O / gate-up / down run as one fused launch each
+    import os
+    if os.environ.get("PF_MLP_FUSED", "0") != "1":
+        assert list(nl) == [P, P * L, P * L, P * (L - 1), P * (L - 1), P * (L - 1), P, 0]
+    else:
+        assert list(nl) == [P, P * L, P * L, 0, 0, 0, P, P * (L - 1)]
+    assert all(ms[c] > 0 for c in range(8) if nl[c])
     res = scorer.score_packed(packed)
     np.testing.assert_array_equal(res.p_yes, direct.p_yes)
 
@@ -416,3 +421,32 @@ def test_full_size_properties_bit_exact():
     sp = scorer.score_packed(pack_requests(split))
     np.testing.assert_array_equal(sp.p_yes, base.p_yes)
     np.testing.assert_array_equal(sp.logits2, base.logits2)
+
+
+def test_fused_layer_tail_bit_identical_to_three_launches(tmp_path):
+    """The fused layer tail (default) and the three-launch path (PF_MLP_FUSED=0, read once per
+    process, so the second pass runs in a subprocess) give bit-identical scores at full C4 width."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "from paper_2510_22101_b200 import CONFIGS, init_device_weights, pack_requests\n"
+        "from paper_2510_22101_b200.engine import PrefillScorer\n"
+        "from tests.synth import make_shared\n"
+        "cfg = CONFIGS['C4'].with_(n_layers=4)\n"
+        "sc = PrefillScorer(init_device_weights(cfg, 0, 'cuda'))\n"
+        "rng = np.random.default_rng(23)\n"
+        "pk = pack_requests([make_shared(rng, 64, list(rng.integers(1, 400, 40)), 'spread'),"
+        " make_shared(rng, 9, [300, 5], 'template')])\n"
+        "r = sc.score_packed(pk)\n"
+        "np.save(sys.argv[1], np.concatenate([r.logits2.ravel(), r.p_yes]))\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        f = str(tmp_path / f"s{flag}.npy")
+        env = dict(os.environ, PF_MLP_FUSED=flag)
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=env, timeout=600)
+        outs.append(np.load(f))
+    np.testing.assert_array_equal(outs[0], outs[1])
