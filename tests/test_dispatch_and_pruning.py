@@ -171,3 +171,20 @@ def test_shard_bounds_balance_tokens_and_cover_items():
             assert len(b) >= 4
         sums = [int(toks[lo:hi].sum()) for lo, hi in b]
         assert max(sums) <= 1000 + int(toks.max())
+
+
+def test_bench_gpus_n_self_launches_torchrun():
+    """`bench.py --gpus N` without a torchrun environment re-runs itself under torch.distributed.run
+    with N ranks (127.0.0.1 rendezvous); rank 0 alone prints the line (reference arm: CPU only)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--config", "C1", "--steps", "1", "--warmup", "1", "--ref-items", "2"],
+                         capture_output=True, text=True, env=env, timeout=600, check=True).stdout
+    lines = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
