@@ -5,7 +5,8 @@ import csv
 import re
 import sys
 
-EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add", "4": "resid-add+norm"}
+EPI = {"0": "bf16", "1": "qkv+rope", "2": "gate/up+swiglu", "3": "resid-add", "4": "resid-add+norm",
+       "100": "resid-add+norm, deep ring (O)"}
 
 
 def main(path):
@@ -16,7 +17,7 @@ def main(path):
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])   # launches, ns, DRAM bytes
     for r in data:
         name = r[ki]
-        m = re.search(r"gemm_bf16_kernel<(?:\(int\))?(\d)", name)
+        m = re.search(r"gemm_bf16_kernel<(?:\(int\))?(\d+)", name)
         key = f"gemm<{EPI.get(m.group(1), m.group(1))}>" if m else re.sub(r"^void |pf::|\(.*", "", name).split("<")[0]
         v = float(r[vi].replace(",", ""))
         if r[mi] == "gpu__time_duration.sum":
