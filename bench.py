@@ -504,8 +504,12 @@ def run_load(args):
     from paper_2510_22101_b200.serving import ScoreCache, ScoringService
 
     cfg = CONFIGS["C4"]
-    n_dev = min(args.gpus, torch.cuda.device_count())
-    scorers = [PrefillScorer(init_device_weights(cfg, 0, f"cuda:{i}"), device=f"cuda:{i}") for i in range(n_dev)]
+    # PF_BENCH_SAME_DEVICE=1: every replica on cuda:0 (exercises the multi-replica path on a one-GPU box;
+    # not a scaling measurement)
+    same = os.environ.get("PF_BENCH_SAME_DEVICE") == "1"
+    n_dev = args.gpus if same else min(args.gpus, torch.cuda.device_count())
+    devs = ["cuda:0"] * n_dev if same else [f"cuda:{i}" for i in range(n_dev)]
+    scorers = [PrefillScorer(init_device_weights(cfg, 0, dv), device=dv) for dv in devs]
     pool = ReplicaPool(scorers, token_budget=args.load_token_budget,
                        shard_tokens=args.c5_shard_tokens, policy=args.c5_policy)
     svc = ScoringService(pool, model_version="c4-seed0", cache=ScoreCache(), workers=args.c5_workers,
@@ -523,7 +527,7 @@ def run_load(args):
 
     for f, _ in issue(3):          # warm-up: kernel attributes, workspaces, pinned pools
         f.result()
-    clocks = ClockSampler(list(range(n_dev)))
+    clocks = ClockSampler(sorted({int(dv.split(":")[1]) for dv in devs}))
     # capacity: a closed-loop burst (every request submitted at once, scored back to back)
     n_cap = max(len(wl.pool), 4 * n_dev)
     t0 = time.perf_counter()
