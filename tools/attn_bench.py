@@ -65,7 +65,7 @@ def main():
         for rows, ref in ref_rows(qkv, packed, H, Hkv, dh, 4):
             err = max(err, float((out[rows].float() - ref).abs().max()))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 50
+        reps = int(os.environ.get("PF_ATTN_REPS", "50"))
         e0.record()
         for _ in range(reps):
             run()
