@@ -161,6 +161,14 @@ PF_API int pf_rmsnorm(const float* x, const float* gamma, void* y_bf16, int T, i
 PF_API int pf_prefix_attention(const void* qkv, void* out, int T, int n_heads, int n_kv_heads,
                         int d_head, const int32_t* segs, const int32_t* work, int n_work,
                         pf_stream_t stream);
+/* Last layer, last-token rows (replaces the tile attention there; pf_score uses it):
+ * out[i, h*dh:(h+1)*dh] = softmax(q_rows[i,h] . K^T / sqrt(dh)) V over row last_idx[i]'s keys (its
+ * segment's shared prefix and its own tokens up to last_idx[i]); K, V = the k/v columns of qkv
+ * ([T x (H+2Hkv)*dh], RoPE applied).  segs ordered by q_off as pf_pack_* emits them.  fp32 math.
+ * max_keys bounds a row's key count (shared memory); a row past it is written as NaN. */
+PF_API int pf_attention_last_rows(const void* q_rows, const void* qkv, int n_heads, int n_kv_heads, int d_head,
+                                  const int32_t* segs, int n_seg, const int32_t* last_idx, int n_items,
+                                  int max_keys, void* out, pf_stream_t stream);
 PF_API int pf_head_last_token(const float* resid, const int32_t* last_idx, int n_items, int d,
                        const float* final_gamma, const float* w_yes, const float* w_no,
                        float eps, float* logits2, float* p_yes, int* bad_flag,

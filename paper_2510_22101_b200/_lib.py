@@ -23,7 +23,7 @@ EPI_BF16, EPI_ROPE_BF16, EPI_SWIGLU, EPI_RESID_ADD, EPI_RESID_ADD_NORM = 0, 1, 2
 EXPORTED_SYMBOLS = (
     "pf_model_create", "pf_model_destroy", "pf_workspace_bytes", "pf_score", "pf_score_host", "pf_score_capture",
     "pf_validate_packed", "pf_layer_tail", "pf_debug_set_mlp_stats",
-    "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_head_last_token",
+    "pf_gemm_bf16", "pf_gemm_bf16_ex", "pf_embed", "pf_rmsnorm", "pf_prefix_attention", "pf_attention_last_rows", "pf_head_last_token",
     "pf_last_error", "pf_version", "pf_debug_set_trace", "pf_profile_enable", "pf_profile_read", "pf_profile_class_name",
     "pf_tokenize", "pf_tokenize_spans", "pf_tokenize_batch", "pf_pack_sizes", "pf_pack_requests",
 )
@@ -100,6 +100,7 @@ _SIGS = {
     "pf_embed": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "pf_rmsnorm": (_I, [_P, _P, _P, _I, _I, _F, _P]),
     "pf_prefix_attention": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _I, _P]),
+    "pf_attention_last_rows": (_I, [_P, _P, _I, _I, _I, _P, _I, _P, _I, _I, _P, _P]),
     "pf_head_last_token": (_I, [_P, _P, _I, _I, _P, _P, _P, _F, _P, _P, _P, _P]),
     "pf_debug_set_trace": (_I, [_P, ctypes.c_uint]),
     "pf_tokenize": (_I, [ctypes.c_char_p, ctypes.c_size_t, _I, _I, _P, ctypes.c_int64, _P]),

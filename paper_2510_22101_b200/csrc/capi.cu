@@ -124,6 +124,8 @@ struct pf_model {
   pf_model_desc d;
   std::vector<const void*> w_qkv, w_o, w_gu, w_down;
   std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;  // cached weight (B operand) maps
+  CUtensorMap tm_q_last, tm_kv_last;                        // last layer: q rows / k,v rows of W_qkv
+  bool last_rows_attention;  // last layer: Q and attention on the last-token rows only (PF_LAST_ROWS_ATTN=0 disables)
   int qkv_n, attn_k;
   bool last_layer_compact;   // PF_NO_LAST_LAYER_COMPACT=1 disables (for tests/benchmarks)
 };
@@ -147,6 +149,9 @@ struct Workspace {
   void* attn_c;      // [n_items x H*dh] bf16  last-layer compacted rows
   void* hi_c;        // [n_items x d] bf16
   void* lo_c;        // [n_items x d] uint8
+  void* q_c;         // [n_items x H*dh] bf16  last layer: q of the last-token rows (RoPE applied)
+  float* ss_c;       // [ss_parts(d) x n_items] their fused-RMSNorm partial sums
+  int32_t* pos_c;    // [n_items] their positions
   // device copies of host inputs/outputs (pf_score_host)
   int32_t *ids, *pos, *segs, *work, *last_idx;
   float *logits2, *p_yes;
@@ -173,6 +178,9 @@ Workspace layout(const pf_model* m, int T, int n_items, int n_seg, int n_work, u
   w.attn_c = take((size_t)n_items * m->attn_k * 2);
   w.hi_c = take((size_t)n_items * d.d_model * 2);
   w.lo_c = take((size_t)n_items * d.d_model);
+  w.q_c = take((size_t)n_items * d.n_heads * d.d_head * 2);
+  w.ss_c = reinterpret_cast<float*>(take((size_t)ss_parts(d.d_model) * n_items * 4));
+  w.pos_c = reinterpret_cast<int32_t*>(take((size_t)n_items * 4));
   w.ids = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.pos = reinterpret_cast<int32_t*>(take((size_t)T * 4));
   w.segs = reinterpret_cast<int32_t*>(take((size_t)n_seg * 16));
@@ -241,6 +249,21 @@ int pf_model_create(const pf_model_desc* desc, pf_model** out) {
               make_weight_tmap(&m->tm_gu[l], m->w_gu[l], 2 * d.d_ff_pad, d.d_model, d.d_model) &&
               make_weight_tmap(&m->tm_down[l], m->w_down[l], d.d_model, d.d_ff_pad, d.d_ff_pad);
     if (!ok) { delete m; return -3; }
+  }
+  {
+    // the split needs the q and k,v widths to be GEMM N multiples (128); otherwise the last layer
+    // runs the full QKV GEMM and tile attention before compacting
+    const int qn = d.n_heads * d.d_head, kvn = m->qkv_n - qn;
+    const char* e = getenv("PF_LAST_ROWS_ATTN");
+    m->last_rows_attention = !(e && e[0] == '0') && qn % 128 == 0 && kvn % 128 == 0 &&
+                             d.n_heads / d.n_kv_heads <= 8;
+    if (m->last_rows_attention &&
+        !(make_weight_tmap(&m->tm_q_last, m->w_qkv[L - 1], qn, d.d_model, d.d_model) &&
+          make_weight_tmap(&m->tm_kv_last, static_cast<const char*>(m->w_qkv[L - 1]) + (size_t)qn * d.d_model * 2,
+                           kvn, d.d_model, d.d_model))) {
+      delete m;
+      return -3;
+    }
   }
   *out = m;
   return 0;
@@ -325,7 +348,7 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
                        int n_seg, const int32_t* work, int n_work, const int32_t* last_idx,
                        int n_items, int T, const Workspace& w, float* logits2, float* p_yes,
                        int* bad, cudaStream_t st, const pf_capture* cap = nullptr) {
-  (void)n_seg;
+
   const pf_model_desc& d = m->d;
   const float eps = d.rms_eps;
   const float inv_d = 1.0f / (float)d.d_model;
@@ -346,6 +369,11 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     if ((rc = launch_rope_gather(pos, d.rope_cos, d.rope_sin, d.d_head / 2, T, w.rope_cs, st))) return rc;
   }
   for (int l = 0; l < d.n_layers; ++l) {
+    // Last layer: only the n_items last-token rows reach the head.  K and V are still needed for every
+    // row, but Q, attention, the O projection and the MLP only for those rows (the per-row arithmetic
+    // of the GEMMs is unchanged; their attention runs in attn_last_rows_kernel, fp32).
+    const bool last = l == d.n_layers - 1 && n_items < T && m->last_layer_compact && cap == nullptr;
+    const bool split_qkv = last && m->last_rows_attention;
     GemmDesc g{};
     g.A = w.xb; g.lda = d.d_model; g.B = d.w_qkv[l]; g.ldb = d.d_model;
     g.C = w.qkv; g.ldc = m->qkv_n; g.M = T; g.N = m->qkv_n; g.K = d.d_model;
@@ -353,23 +381,47 @@ static int run_forward(pf_model* m, const int32_t* ids, const int32_t* pos, cons
     g.rope_heads = d.n_heads + d.n_kv_heads; g.rope_dh = d.d_head; g.max_seq = d.max_seq;
     g.rope_cs = w.rope_cs;
     g.row_ss = w.ss_attn; g.ss_ld = T; g.inv_d = inv_d; g.eps = eps;
-    {
-      PF_PROF(PF_PROF_QKV);
-      if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
-    }
-    AttnDesc a{};
-    a.qkv = w.qkv; a.out = w.attn; a.T = T; a.H = d.n_heads; a.Hkv = d.n_kv_heads; a.dh = d.d_head;
-    a.work = work; a.n_work = n_work; a.segs = segs; a.scale = 1.0f / sqrtf((float)d.d_head);
-    {
+    if (split_qkv) {
+      const int qn = d.n_heads * d.d_head;
+      {
+        PF_PROF(PF_PROF_QKV);
+        // K and V of every row: the weight rows after the q heads, written into the qkv buffer's k/v columns
+        GemmDesc kv = g;
+        kv.B = static_cast<const char*>(d.w_qkv[l]) + (size_t)qn * d.d_model * 2;
+        kv.C = static_cast<char*>(w.qkv) + (size_t)qn * 2;
+        kv.N = m->qkv_n - qn;
+        kv.rope_heads = d.n_kv_heads;
+        if ((rc = launch_gemm(kv, &m->tm_kv_last, st))) return rc;
+        // q of the last-token rows
+        if ((rc = launch_gather_q_rows(last_idx, n_items, w.xb, d.d_model, w.ss_attn, T, pos, w.hi_c, w.ss_c,
+                                       w.pos_c, st)))
+          return rc;
+        GemmDesc q = g;
+        q.A = w.hi_c; q.M = n_items; q.N = qn; q.C = w.q_c; q.ldc = qn;
+        q.pos = w.pos_c; q.rope_cs = nullptr; q.rope_heads = d.n_heads;
+        q.row_ss = w.ss_c; q.ss_ld = n_items;
+        if ((rc = launch_gemm(q, &m->tm_q_last, st))) return rc;
+      }
+      PF_PROF(PF_PROF_ATTENTION);
+      if ((rc = launch_attention_last_rows(w.q_c, w.qkv, m->qkv_n, segs, n_seg, last_idx, n_items, d.n_heads,
+                                           d.n_kv_heads, d.d_head, d.max_seq, w.attn_c, st)))
+        return rc;
+    } else {
+      {
+        PF_PROF(PF_PROF_QKV);
+        if ((rc = launch_gemm(g, &m->tm_qkv[l], st))) return rc;
+      }
+      AttnDesc a{};
+      a.qkv = w.qkv; a.out = w.attn; a.T = T; a.H = d.n_heads; a.Hkv = d.n_kv_heads; a.dh = d.d_head;
+      a.work = work; a.n_work = n_work; a.segs = segs; a.scale = 1.0f / sqrtf((float)d.d_head);
       PF_PROF(PF_PROF_ATTENTION);
       if ((rc = launch_attention(a, st))) return rc;
     }
-    if (l == d.n_layers - 1 && n_items < T && m->last_layer_compact && cap == nullptr) {
-      // Last layer: only the n_items last-token rows reach the head, so the O-projection and MLP
-      // run on those rows alone (per-row arithmetic unchanged; tests check bit-equality).
+    if (last) {
+      // O-projection and MLP on the n_items last-token rows alone
       PF_PROF(PF_PROF_LAST_LAYER);
-      if ((rc = launch_gather_rows(last_idx, n_items, w.attn, m->attn_k, w.xb, w.rlo, d.d_model, w.attn_c,
-                                   w.hi_c, w.lo_c, st)))
+      if ((rc = launch_gather_rows(last_idx, n_items, split_qkv ? nullptr : w.attn, split_qkv ? 0 : m->attn_k,
+                                   w.xb, w.rlo, d.d_model, w.attn_c, w.hi_c, w.lo_c, st)))
         return rc;
       GemmDesc o{};
       o.A = w.attn_c; o.lda = m->attn_k; o.B = d.w_o[l]; o.ldb = m->attn_k;
@@ -643,6 +695,16 @@ int pf_prefix_attention(const void* qkv, void* out, int T, int n_heads, int n_kv
   a.qkv = qkv; a.out = out; a.T = T; a.H = n_heads; a.Hkv = n_kv_heads; a.dh = d_head;
   a.segs = segs; a.work = work; a.n_work = n_work; a.scale = 1.0f / sqrtf((float)d_head);
   return launch_attention(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pf_attention_last_rows(const void* q_rows, const void* qkv, int n_heads, int n_kv_heads, int d_head,
+                           const int32_t* segs, int n_seg, const int32_t* last_idx, int n_items, int max_keys,
+                           void* out, pf_stream_t stream) {
+  if (!q_rows || !qkv || !segs || !last_idx || !out) return fail(-1, "pf_attention_last_rows: null buffer");
+  if (n_heads < 1 || n_kv_heads < 1) return fail(-2, "pf_attention_last_rows: bad head counts");
+  return launch_attention_last_rows(q_rows, qkv, (n_heads + 2 * n_kv_heads) * d_head, segs, n_seg, last_idx,
+                                    n_items, n_heads, n_kv_heads, d_head, max_keys, out,
+                                    reinterpret_cast<cudaStream_t>(stream));
 }
 
 int pf_head_last_token(const float* resid, const int32_t* last_idx, int n_items, int d,

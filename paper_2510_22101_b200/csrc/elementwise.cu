@@ -151,6 +151,252 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restr
   for (int j = lane; j < resid_v4 / 2; j += 32) lo_c[(size_t)i * resid_v4 / 2 + j] = __ldg(lo + r * resid_v4 / 2 + j);
 }
 
+// ---------------------------------------------------------------- last layer, last-token rows
+// Only the n_items last-token rows of the last layer reach the head, so that layer needs K and V for
+// every packed row but Q, attention, O and the MLP only for those rows.  gather_q_rows collects the
+// Q GEMM's inputs for them: the residual hi row, its fused-RMSNorm partial sums ([parts][T] ->
+// [parts][n]) and its position (RoPE).
+__global__ void __launch_bounds__(256) gather_q_rows_kernel(const int32_t* __restrict__ last_idx, int n,
+                                                            const uint4* __restrict__ hi, int resid_v4,
+                                                            const float* __restrict__ ss, int parts, int T,
+                                                            const int32_t* __restrict__ pos,
+                                                            uint4* __restrict__ hi_c, float* __restrict__ ss_c,
+                                                            int32_t* __restrict__ pos_c) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const size_t r = (size_t)__ldg(last_idx + i);
+  for (int j = lane; j < resid_v4; j += 32) hi_c[(size_t)i * resid_v4 + j] = __ldg(hi + r * resid_v4 + j);
+  for (int p = lane; p < parts; p += 32) ss_c[(size_t)p * n + i] = __ldg(ss + (size_t)p * T + r);
+  if (lane == 0) pos_c[i] = __ldg(pos + r);
+}
+
+int launch_gather_q_rows(const int32_t* last_idx, int n, const void* hi, int d, const float* ss, int T,
+                         const int32_t* pos, void* hi_c, float* ss_c, int32_t* pos_c, cudaStream_t stream) {
+  if (n == 0) return 0;
+  gather_q_rows_kernel<<<(n + 7) / 8, 256, 0, stream>>>(last_idx, n, reinterpret_cast<const uint4*>(hi), d / 8, ss,
+                                                        ss_parts(d), T, pos, reinterpret_cast<uint4*>(hi_c), ss_c,
+                                                        pos_c);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "gather_q launch: %s", cudaGetErrorString(e));
+}
+
+// Attention of one query row per item (its last token) against the item's keys: the shared prefix
+// [kv_off, kv_off + kv_len) and its own tokens up to the row (SPEC.md:249-272 at the rows that reach
+// the head).  One CTA per (item, kv head): the r = H / Hkv query heads of the GQA group share every
+// K/V row loaded.  fp32 scores, exact expf, fp32 P and accumulation (the tile kernel's P is bf16).
+// The row's segment is the last one with q_off <= row (segs are ordered by q_off, as the packer emits
+// them): counted by the whole CTA, one load per thread per 256 segments (a binary search would be a
+// chain of dependent global loads).  HBM-bound at long items: each CTA streams its item's K and V once,
+// 8 keys in flight per thread in the P.V loop.
+// A key count above l_max (max_seq, the smem bound) writes NaN: the head's non-finite flag reports it.
+constexpr int LR_THREADS = 256;
+constexpr int LR_WARPS = LR_THREADS / 32;
+constexpr int LR_MAX_R = 8;
+template <int DH>
+__global__ void __launch_bounds__(LR_THREADS) attn_last_rows_kernel(const __nv_bfloat16* __restrict__ q_c,
+                                                                   const __nv_bfloat16* __restrict__ qkv, int qkv_n,
+                                                                   const int4* __restrict__ segs, int n_seg,
+                                                                   const int32_t* __restrict__ last_idx, int H,
+                                                                   int Hkv, float scale, int l_max,
+                                                                   __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float lr_sm[];   // q [r][4][DH/4 + 4] (pre-scaled), p [r][l_max], PV partials [8][r][DH]
+  __shared__ float red[LR_MAX_R][LR_WARPS];
+  __shared__ float inv[LR_MAX_R];
+  pdl_launch_dependents();
+  pdl_wait();
+  const int i = blockIdx.x, g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int r = H / Hkv;
+  const int row = __ldg(last_idx + i);
+  int cnt = 0;
+  for (int k0 = 0; k0 < n_seg; k0 += LR_THREADS) {
+    const int k = k0 + tid;
+    cnt += __syncthreads_count(k < n_seg && __ldg(&segs[k].z) <= row);
+  }
+  const int4 sg = segs[max(cnt - 1, 0)];
+  const int kv_len = sg.y;
+  const int L = kv_len + (row - sg.z + 1);
+  __nv_bfloat16* orow = out + (size_t)i * H * DH + (size_t)g * r * DH;
+  if (L < 1 || L > l_max) {
+    for (int e = tid; e < r * DH; e += LR_THREADS) orow[e] = __float2bfloat16(__int_as_float(0x7fc00000));
+    return;
+  }
+  float* qs = lr_sm;
+  float* ps = lr_sm + r * (DH + 16);
+  const __nv_bfloat16* qrow = q_c + (size_t)i * H * DH + (size_t)g * r * DH;
+  for (int e = tid; e < r * DH; e += LR_THREADS) {   // [h][quarter][DH/4 + 4 pad]
+    const int h = e / DH, c = e % DH;
+    qs[h * (DH + 16) + (c / (DH / 4)) * (DH / 4 + 4) + c % (DH / 4)] = __bfloat162float(qrow[e]) * scale;
+  }
+  __syncthreads();
+  const size_t kcol = (size_t)(H + g) * DH, vcol = (size_t)(H + Hkv + g) * DH;
+  auto key_row = [&](int j) { return (size_t)(j < kv_len ? sg.x + j : sg.z + (j - kv_len)); };
+  // scores: four lanes per key, eight keys per warp step; lane (k, sub) reads DH/4 columns of key k's
+  // K row (64 contiguous bytes: a warp load touches 8 rows, not 32) against the same q columns, kept
+  // in smem with a 4-float pad per quarter so the four quarters hit different banks
+  constexpr int VPL = DH / 32;
+  constexpr int QD = DH / 4;
+  auto load_row = [&](const __nv_bfloat16* p, float (&v)[VPL]) {
+    if constexpr (VPL == 4) {
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+      const float2 a = __bfloat1622float2(__ldg(reinterpret_cast<const __nv_bfloat162*>(p)));
+      v[0] = a.x; v[1] = a.y;
+    }
+  };
+  {
+    const int sub = lane & 3;
+    const float* qsub = qs + sub * (QD + 4);
+#pragma unroll 2
+    for (int j0 = wid * 8; j0 < L; j0 += LR_WARPS * 8) {
+      const int j = j0 + (lane >> 2);
+      float acc[LR_MAX_R];
+#pragma unroll
+      for (int h = 0; h < LR_MAX_R; ++h) acc[h] = 0.f;
+      if (j < L) {
+        const uint4* kp = reinterpret_cast<const uint4*>(qkv + key_row(j) * qkv_n + kcol + sub * QD);
+        uint4 ku[QD / 8];
+#pragma unroll
+        for (int c = 0; c < QD / 8; ++c) ku[c] = __ldg(kp + c);
+#pragma unroll
+        for (int c = 0; c < QD / 8; ++c) {
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&ku[c]);
+          float kf[8];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(b2[e]);
+            kf[2 * e] = f.x;
+            kf[2 * e + 1] = f.y;
+          }
+#pragma unroll
+          for (int h = 0; h < LR_MAX_R; ++h) {
+            if (h >= r) break;
+            const float4 qa = *reinterpret_cast<const float4*>(qsub + h * 4 * (QD + 4) + 8 * c);
+            const float4 qb = *reinterpret_cast<const float4*>(qsub + h * 4 * (QD + 4) + 8 * c + 4);
+            acc[h] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] + qb.y * kf[5] +
+                      qb.z * kf[6] + qb.w * kf[7];
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < LR_MAX_R; ++h) {
+        if (h >= r) break;
+        acc[h] += __shfl_xor_sync(0xffffffffu, acc[h], 1);
+        acc[h] += __shfl_xor_sync(0xffffffffu, acc[h], 2);
+        if (sub == 0 && j < L) ps[h * l_max + j] = acc[h];
+      }
+    }
+  }
+  __syncthreads();
+  // softmax per head (block reductions through red[][])
+#pragma unroll
+  for (int h = 0; h < LR_MAX_R; ++h) {
+    if (h >= r) break;
+    float m = -INFINITY;
+    for (int j = tid; j < L; j += LR_THREADS) m = fmaxf(m, ps[h * l_max + j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[h][wid] = m;
+    __syncthreads();
+    m = red[h][0];
+#pragma unroll
+    for (int w = 1; w < LR_WARPS; ++w) m = fmaxf(m, red[h][w]);
+    __syncthreads();
+    float sum = 0.f;
+    for (int j = tid; j < L; j += LR_THREADS) {
+      const float p = expf(ps[h * l_max + j] - m);
+      ps[h * l_max + j] = p;
+      sum += p;
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) red[h][wid] = sum;
+    __syncthreads();
+    if (tid == 0) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < LR_WARPS; ++w) t += red[h][w];
+      inv[h] = 1.f / t;
+    }
+  }
+  // O = P V / l: warp w takes keys w, w + 8, ...; lane l holds DH/32 consecutive columns (one 8- or
+  // 4-byte load per key, a warp reads the whole V row); the eight warps' partial sums meet in smem
+  float o[LR_MAX_R][VPL];
+#pragma unroll
+  for (int h = 0; h < LR_MAX_R; ++h)
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) o[h][e] = 0.f;
+#pragma unroll 8
+  for (int j = wid; j < L; j += LR_WARPS) {
+    float v[VPL];
+    load_row(qkv + key_row(j) * qkv_n + vcol + lane * VPL, v);
+#pragma unroll
+    for (int h = 0; h < LR_MAX_R; ++h) {
+      if (h >= r) break;
+      const float p = ps[h * l_max + j];
+#pragma unroll
+      for (int e = 0; e < VPL; ++e) o[h][e] = fmaf(p, v[e], o[h][e]);
+    }
+  }
+  float* part = ps + r * l_max;   // [LR_WARPS][r][DH]
+#pragma unroll
+  for (int h = 0; h < LR_MAX_R; ++h) {
+    if (h >= r) break;
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) part[(wid * r + h) * DH + lane * VPL + e] = o[h][e];
+  }
+  __syncthreads();
+  for (int e = tid; e < r * DH; e += LR_THREADS) {
+    const int h = e / DH;
+    float sum = 0.f;
+#pragma unroll
+    for (int w = 0; w < LR_WARPS; ++w) sum += part[w * r * DH + e];
+    orow[e] = __float2bfloat16(sum * inv[h]);
+  }
+}
+
+int launch_attention_last_rows(const void* q_c, const void* qkv, int qkv_n, const int32_t* segs, int n_seg,
+                               const int32_t* last_idx, int n_items, int H, int Hkv, int dh, int l_max,
+                               void* out, cudaStream_t stream) {
+  if (n_items == 0) return 0;
+  if (dh != 128 && dh != 64) return fail(-2, "last-row attention: d_head must be 64 or 128 (got %d)", dh);
+  if (H % Hkv != 0 || H / Hkv > LR_MAX_R)
+    return fail(-2, "last-row attention: n_heads / n_kv_heads must divide and be <= %d", LR_MAX_R);
+  if (n_seg < 1 || l_max < 1) return fail(-2, "last-row attention: empty segment table or l_max");
+  const int r = H / Hkv;
+  const size_t smem = (size_t)r * ((1 + LR_WARPS) * dh + 16 + l_max) * sizeof(float);
+  if (smem > 200 * 1024) return fail(-2, "last-row attention: %zu B of shared memory (l_max %d)", smem, l_max);
+  const int dev = current_device();
+  static size_t attr_bytes[kMaxDevices][2] = {};
+  const int ti = dh == 128 ? 0 : 1;
+  if (smem > 48 * 1024 && attr_bytes[dev][ti] < smem) {
+    cudaError_t e = dh == 128 ? cudaFuncSetAttribute(attn_last_rows_kernel<128>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                              : cudaFuncSetAttribute(attn_last_rows_kernel<64>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(-4, "last-row attention smem attr: %s", cudaGetErrorString(e));
+    attr_bytes[dev][ti] = smem;
+  }
+  const dim3 grid(n_items, Hkv);
+  const float scale = 1.0f / sqrtf((float)dh);
+  const auto* qc = reinterpret_cast<const __nv_bfloat16*>(q_c);
+  const auto* kv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  const auto* sg = reinterpret_cast<const int4*>(segs);
+  auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+  if (dh == 128)
+    attn_last_rows_kernel<128><<<grid, LR_THREADS, smem, stream>>>(qc, kv, qkv_n, sg, n_seg, last_idx, H, Hkv, scale,
+                                                                   l_max, o);
+  else
+    attn_last_rows_kernel<64><<<grid, LR_THREADS, smem, stream>>>(qc, kv, qkv_n, sg, n_seg, last_idx, H, Hkv, scale,
+                                                                  l_max, o);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail(-4, "last-row attention launch: %s", cudaGetErrorString(e));
+}
+
 int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const void* hi,
                        const void* lo, int d, void* attn_c, void* hi_c, void* lo_c, cudaStream_t stream) {
   if (n == 0) return 0;

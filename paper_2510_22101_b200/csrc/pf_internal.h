@@ -90,6 +90,11 @@ int launch_rope_gather(const int32_t* pos, const float* cos_tab, const float* si
 inline size_t rope_gather_floats(int T, int half) { return (size_t)((T + 31) / 32) * 32 * 2 * half; }
 int launch_capture_rows(const int32_t* rows, int n, const void* hi, const void* lo, const float* ss, int ss_ld,
                         const float* g, int d, float eps, float* out, cudaStream_t stream);
+int launch_gather_q_rows(const int32_t* last_idx, int n, const void* hi, int d, const float* ss, int T,
+                         const int32_t* pos, void* hi_c, float* ss_c, int32_t* pos_c, cudaStream_t stream);
+int launch_attention_last_rows(const void* q_c, const void* qkv, int qkv_n, const int32_t* segs, int n_seg,
+                               const int32_t* last_idx, int n_items, int H, int Hkv, int dh, int l_max,
+                               void* out, cudaStream_t stream);
 int launch_gather_rows(const int32_t* last_idx, int n, const void* attn, int attn_cols, const void* hi,
                        const void* lo, int d, void* attn_c, void* hi_c, void* lo_c, cudaStream_t stream);
 // resid (fp32) or, when resid == nullptr, the bf16 (hi, lo) pair

@@ -325,6 +325,37 @@ def test_gemm_rope_gathered_table(lib, M, H, Hkv, K, dh):
     torch.testing.assert_close(C.float(), ref, rtol=1.6e-2, atol=2e-2)
 
 
+@pytest.mark.parametrize("H,Hkv,dh", [(2, 1, 128), (10, 5, 128), (4, 2, 64), (8, 1, 128), (3, 3, 64)])
+def test_attention_last_rows(lib, H, Hkv, dh):
+    """The last layer's attention of the last-token rows only (fp32) against the torch fp32
+    reference of the full ragged attention at those rows: shared prefixes of 64 / 5 / 0 / 200 tokens,
+    items of 1-300 tokens."""
+    rng = np.random.default_rng(5)
+    reqs = [
+        SharedBatch(list(rng.integers(16, 100, 64)), [list(rng.integers(16, 100, s)) for s in (100, 128, 200, 1, 300)]),
+        SharedBatch(list(rng.integers(16, 100, 5)), [list(rng.integers(16, 100, 130))]),
+        SharedBatch([], [list(rng.integers(16, 100, 7)), list(rng.integers(16, 100, 129))]),
+        SharedBatch(list(rng.integers(16, 100, 200)), [list(rng.integers(16, 100, 3))]),
+    ]
+    packed = pack_requests(reqs)
+    T, n = packed.T, len(packed.last_idx)
+    qkv = rand_bf16(T, (H + 2 * Hkv) * dh, seed=21)
+    last = torch.from_numpy(packed.last_idx.astype(np.int32)).cuda()
+    q_rows = qkv[last.long(), : H * dh].contiguous()
+    out = torch.full((n, H * dh), float("nan"), device="cuda", dtype=torch.bfloat16)
+    segs = torch.from_numpy(packed.segs).cuda()
+    _lib.check(lib.pf_attention_last_rows(P(q_rows), P(qkv), H, Hkv, dh, P(segs), len(packed.segs), P(last), n,
+                                          2048, P(out), stream()))
+    torch.cuda.synchronize()
+    ref = attention_ref(qkv, packed, H, Hkv, dh)[last.long()]
+    torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=1e-2)
+    # a key count past max_keys is reported as NaN rows (the head's non-finite flag), not read past smem
+    _lib.check(lib.pf_attention_last_rows(P(q_rows), P(qkv), H, Hkv, dh, P(segs), len(packed.segs), P(last), n,
+                                          6, P(out), stream()))
+    torch.cuda.synchronize()
+    assert bool(torch.isnan(out.float()).any(dim=1).all())
+
+
 def test_prefix_attention_rescales_and_masked_blocks(lib):
     """Online softmax under large score swings (the lazy rescale of O in TMEM fires when the running
     max grows by > 2^8) and items long enough that whole warps see fully masked 32-key halves."""
