@@ -267,12 +267,22 @@ def run_ours(args):
     pp = PinnedPacked(packed)
     n_items = packed.n_items
     flops_step = algorithmic_flops(cfg, shape.prefix_len, [shape.suffix_len] * shape.n_items) * shape.n_requests
-    # executed work: the last layer's O-projection + MLP run on the n_items last-token rows only
-    flops_exec = flops_step - shape.n_requests * (packed.T // shape.n_requests - shape.n_items) * 2 * (
-        cfg.q_width * cfg.d_model + 3 * cfg.d_model * cfg.d_ff)
+    # executed work: the last layer's Q projection, attention, O-projection and MLP run on the n_items
+    # last-token rows only (K/V still for every row)
+    last_rows = os.environ.get("PF_LAST_ROWS_ATTN", "1") != "0"
+    non_last = shape.n_requests * (packed.T // shape.n_requests - shape.n_items)
+    flops_exec = flops_step - non_last * 2 * (cfg.q_width * cfg.d_model + 3 * cfg.d_model * cfg.d_ff)
+    if last_rows:
+        P_, S_ = shape.prefix_len, shape.suffix_len
+        pairs_layer = P_ * (P_ + 1) / 2 + shape.n_items * (S_ * P_ + S_ * (S_ + 1) / 2)
+        pairs_last = shape.n_items * (P_ + S_)
+        flops_exec -= shape.n_requests * (non_last * 2 * cfg.d_model * cfg.q_width
+                                          + 4 * cfg.n_heads * cfg.d_head * (pairs_layer - pairs_last))
     # embed + rope-gather + (L-1) x [QKV, attention, O, gate/up, down | QKV, attention, fused tail] + last
-    # layer [QKV, attention, gather, O, gate/up, down] + head  (RMSNorm is fused into the GEMM epilogues)
-    launches = lambda fused: (3 if fused else 5) * (cfg.n_layers - 1) + 6 + 3
+    # layer [QKV, attention, gather, O, gate/up, down] + head  (RMSNorm is fused into the GEMM epilogues);
+    # with the last-row split the last layer's QKV + attention are K/V GEMM, q gather, Q GEMM, last-row
+    # attention (+2)
+    launches = lambda fused: (3 if fused else 5) * (cfg.n_layers - 1) + 6 + 3 + (2 if last_rows else 0)
 
     def barrier():
         if ws > 1:

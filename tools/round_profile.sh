@@ -6,7 +6,7 @@ for c in C4 C2 C3; do timeout 600 python bench.py --config $c > $out/bench_$c.js
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
 K='regex:gemm|attn|embed|head|gather|rope'
 for c in C4 C2; do
-  timeout 600 ncu --metrics $M --clock-control none -k "$K" -s 144 -c 144 --csv --log-file $out/launches_$c.csv \
+  timeout 600 ncu --metrics $M --clock-control none -k "$K" -s 146 -c 146 --csv --log-file $out/launches_$c.csv \
     python tools/profile_step.py --config $c > /dev/null 2>&1
   python tools/launch_breakdown.py $out/launches_$c.csv > $out/launch_breakdown_$c.txt 2>&1
 done
