@@ -57,7 +57,10 @@ def test_capture_matches_oracle(name):
         assert err <= TOL_CAPTURE
 
 
-def test_capture_deterministic_and_scores_unchanged():
+def test_capture_deterministic_and_scores_unchanged(monkeypatch):
+    """Captured rows are deterministic and independent of the launch split; a capturing pass runs
+    every row through every layer, so its scores equal the uncompacted forward bit for bit (and the
+    default forward, whose last layer runs on the last-token rows only, within 2e-3)."""
     cfg = CONFIGS["TINY_GQA"]
     scorer = PrefillScorer(init_weights(cfg, 0))
     prompts = prompts_for(2, 8)
@@ -74,7 +77,11 @@ def test_capture_deterministic_and_scores_unchanged():
     gains = torch.stack([g.float() for g in scorer.weights.ln_mlp])
     out, logits2, _ = scorer.score_capture(dp, rows, gains, return_scores=True)
     assert out.shape == (cfg.n_layers, packed.T, cfg.d_model)
-    np.testing.assert_array_equal(logits2.cpu().numpy(), plain.logits2)
+    monkeypatch.setenv("PF_NO_LAST_LAYER_COMPACT", "1")
+    full = PrefillScorer(scorer.weights).score_packed(packed)
+    np.testing.assert_array_equal(logits2.cpu().numpy(), full.logits2)
+    p_cap = 1.0 / (1.0 + np.exp(-(logits2.cpu().numpy()[:, 0] - logits2.cpu().numpy()[:, 1])))
+    assert np.max(np.abs(p_cap - plain.p_yes)) <= 2e-3
 
 
 def test_capture_then_calibrated_prune_parity():
