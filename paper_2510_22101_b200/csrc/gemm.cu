@@ -57,6 +57,13 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 // and a 4-deep ring, so a tile's whole residual (4 chunks) is requested while its MMAs run.  At K >= 2048
 // the fifth mainloop stage is worth more (tools/gemm_bench.py: C4 O 127.5 -> 123.4 us, C2 O 113 -> 116).
 constexpr int EPI_RESID_ADD_NORM_DEEP = 100;
+// (A/B knobs; at the C4 O shape 4 + 4 beats 5 + 2: 118 vs 122.5 us alone, tools/gemm_bench.py)
+#ifndef PF_DEEP_STAGES
+#define PF_DEEP_STAGES 4
+#endif
+#ifndef PF_DEEP_RBD
+#define PF_DEEP_RBD 4
+#endif
 #ifndef PF_DEEP_RING_MAX_K
 #define PF_DEEP_RING_MAX_K 1536
 #endif
@@ -69,10 +76,11 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
   static constexpr bool DEEP = EPI == EPI_RESID_ADD_NORM_DEEP;
   static constexpr bool RING = EPI == EPI_RESID_ADD_NORM || DEEP;
-  static constexpr int RBD = DEEP ? 4 : PF_RB_DEPTH;         // ring depth (chunks in flight per warp)
+  static constexpr int RBD = DEEP ? PF_DEEP_RBD : PF_RB_DEPTH;   // ring depth (chunks in flight per warp)
+  static_assert(!RING || RBD >= 2, "the residual ring recycles slot k-2: depth >= 2");
   static constexpr bool ROPE = EPI == EPI_ROPE_BF16;
   // the RoPE epilogue stages a whole 256-column tile (4 boxes per warp) and gives up a stage for it
-  static constexpr int STAGES = DEEP ? 4 : RING ? PF_RING_STAGES : ROPE ? (CG == 2 ? 5 : 3) : (CG == 2 ? PF_PLAIN_STAGES : 4);
+  static constexpr int STAGES = DEEP ? PF_DEEP_STAGES : RING ? PF_RING_STAGES : ROPE ? (CG == 2 ? 5 : 3) : (CG == 2 ? PF_PLAIN_STAGES : 4);
   // ring: RBD (hi, lo) chunk slots per epilogue warp; otherwise 2 (RoPE: 4) staging boxes per warp
   static constexpr int EPI_BYTES = RING ? 4 * RBD * RB_SLOT : 4 * (ROPE ? 4 : 2) * GEMM_STG_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
