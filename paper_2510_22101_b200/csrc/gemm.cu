@@ -380,7 +380,11 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
           cs4 = reinterpret_cast<const float4*>(args.rope_cos + (size_t)p * half);
           sn4 = reinterpret_cast<const float4*>(args.rope_sin + (size_t)p * half);
         }
+#ifdef PF_DEBUG_ROPE_NO_TABLE   // A/B timing only (wrong results): the RoPE epilogue without table reads
+        const bool row_rot = false;
+#else
         const bool row_rot = r0 < args.M;   // rows past M are padding (the gathered table ends there)
+#endif
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           cv[j4] = row_rot ? __ldg(cs4 + j4 * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
@@ -547,7 +551,11 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
         const int hd0 = ((int)warp - 2) / 4 * hpw;    // first head of this warp
         const int box0 = hd0 * dh / 64;               // first 64-column staging box of this warp
         const int n_items = cpb * hpw;
+#ifdef PF_DEBUG_ROPE_NO_TABLE
+        const bool row_rot = false;
+#else
         const bool row_rot = r0 < args.M;   // rows past M are padding (the gathered table ends there)
+#endif
         const uint32_t stg0 = smem_u32(my_stg);
         uint32_t x1[32], x2[32];
         tmem_ld_32x32b_x32(t_row + hd0 * dh, x1);
