@@ -596,6 +596,8 @@ static int validate_packed(const pf_model* m, const int32_t* ids, const int32_t*
     const int64_t kv_end = (int64_t)g[0] + g[1], q_end = (int64_t)g[2] + g[3];
     if (g[0] < 0 || g[1] < 0 || g[2] < 0 || g[3] < 1 || kv_end > T || q_end > T)
       return fail(-1, "segment %d {%d,%d,%d,%d} outside [0,%d)", s, g[0], g[1], g[2], g[3], T);
+    if (s > 0 && g[2] < (int64_t)g[-2] + g[-1])   // q ranges increase (the last-row attention relies on it)
+      return fail(-1, "segment %d q range [%d,+%d) overlaps or precedes segment %d", s, g[2], g[3], s - 1);
   }
   for (int w = 0; w < n_work; ++w) {
     const int32_t* k = work + 4 * w;

@@ -498,6 +498,10 @@ __global__ void __launch_bounds__(256) validate_packed_kernel(
       const int4 g = __ldg(segs + idx);
       if (g.x < 0 || g.y < 0 || g.z < 0 || g.w < 1 || (long long)g.x + g.y > T || (long long)g.z + g.w > T)
         code = PF_BAD_SEG;
+      if (idx > 0) {   // q ranges increase and do not overlap (the packer's order)
+        const int4 p = __ldg(segs + idx - 1);
+        if ((long long)g.z < (long long)p.z + p.w) code = PF_BAD_SEG;
+      }
     } else if ((idx -= n_seg) < n_work) {
       const int4 k = __ldg(work + idx);
       if (k.x < 0 || k.x >= n_seg || k.y < 0 || (long long)k.y * 128 >= __ldg(segs + k.x).w) code = PF_BAD_WORK;

@@ -356,6 +356,9 @@ def validate_packed(packed: PackedBatch, cfg: ModelConfig) -> None:
     if ((segs[:, :3] < 0).any() or (segs[:, 3] < 1).any() or (segs[:, 0] + segs[:, 1] > T).any()
             or (segs[:, 2] + segs[:, 3] > T).any()):
         raise ValueError("segment outside [0, T)")
+    if (segs[1:, 2] < segs[:-1, 2] + segs[:-1, 3]).any():
+        # the packer's order; the last layer finds a last-token row's segment by its q offset
+        raise ValueError("segments out of order (q ranges must increase and not overlap)")
     if (work[:, 0] < 0).any() or (work[:, 0] >= len(segs)).any() or (work[:, 1] < 0).any():
         raise ValueError("work tile names a missing segment")
     if (work[:, 1] * 128 >= segs[work[:, 0], 3]).any():

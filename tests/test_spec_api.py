@@ -68,7 +68,7 @@ def _good():
 
 @pytest.mark.parametrize("field,index,value", [
     ("ids", (0,), 40000), ("ids", (3,), -1), ("pos", (2,), 2048), ("pos", (1,), -5),
-    ("segs", (1, 3), 0), ("segs", (1, 2), 10 ** 6), ("segs", (0, 1), -1),
+    ("segs", (1, 3), 0), ("segs", (1, 2), 10 ** 6), ("segs", (0, 1), -1), ("segs", (2, 2), 1),
     ("work", (0, 0), 99), ("work", (0, 1), 7), ("last_idx", (1,), 10 ** 6), ("last_idx", (0,), -1)])
 def test_host_validation_rejects_each_malformed_field(field, index, value):
     cfg = CONFIGS["TINY"]
@@ -190,7 +190,7 @@ def test_device_bounds_check_rejects_malformed_device_batches():
     scorer = PrefillScorer(init_weights(CONFIGS["TINY"], 0))
     good = _good()
     scorer.validate_device(DevicePacked(good, scorer.device))
-    for field, index, value in [("ids", (0,), 40000), ("pos", (2,), 2048), ("segs", (1, 3), 0),
+    for field, index, value in [("ids", (0,), 40000), ("pos", (2,), 2048), ("segs", (1, 3), 0), ("segs", (2, 2), 1),
                                 ("work", (0, 0), 99), ("last_idx", (1,), 10 ** 6)]:
         pk = _good()
         getattr(pk, field)[index] = value
