@@ -67,6 +67,8 @@ typedef struct pf_model_desc {
  *   segs[n_seg][4]           {kv_off, kv_len, q_off, q_len}: query rows [q_off, q_off+q_len) attend
  *                            densely to rows [kv_off, kv_off+kv_len) (the shared prefix) and
  *                            causally to themselves.  A request's prefix is {q_off, 0, q_off, P}.
+ *                            Segments are ordered by q_off with non-overlapping q ranges (as
+ *                            pf_pack_requests emits them; the validators reject anything else).
  *   work[n_work][4]          {seg, q_tile, 0, 0}: one entry per 128-row query tile of a segment
  *   last_idx[n_items]        packed row of each item's last token
  */
