@@ -58,6 +58,14 @@ constexpr int GEMM_STG_BYTES = 32 * 128;              // one 32-row x 128 B stag
 // the fifth mainloop stage is worth more (tools/gemm_bench.py: C4 O 127.5 -> 123.4 us, C2 O 113 -> 116).
 constexpr int EPI_RESID_ADD_NORM_DEEP = 100;
 // (A/B knobs; at the C4 O shape 4 + 4 beats 5 + 2: 118 vs 122.5 us alone, tools/gemm_bench.py)
+// A tile's residual chunks are requested once its accumulator is ready, not while its MMAs run: the
+// residual TMA traffic then no longer competes with the mainloop's operand loads (round 2,
+// tools/gemm_bench.py: C4 O + norm 118.0 -> 115.9 us, C2 O 108.6 -> 107.9, down unchanged; the
+// epilogue warps had slack, ncu shows them waiting for the accumulator 22% of the time).
+// PF_RING_LATE=0 restores the prefetch during the previous tile's epilogue.
+#ifndef PF_RING_LATE
+#define PF_RING_LATE 1
+#endif
 #ifndef PF_DEEP_STAGES
 #define PF_DEEP_STAGES 4
 #endif
@@ -336,12 +344,12 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
       ++ring_issued;
     };
     auto ring_chunks = [&](int t) { return min(GEMM_BN / 64, (args.N - (t % args.num_n_blk) * GEMM_BN) / 64); };
-    // tile t's first RBD chunks go straight into the ring (issued while its MMAs run).  An
-    // extra L2 prefetch of the remaining chunks was measured to make no difference.
+    // tile t's first RBD chunks go straight into the ring (once its accumulator is ready, PF_RING_LATE;
+    // else while its MMAs run).  An extra L2 prefetch of the remaining chunks made no difference.
     auto ring_start = [&](int t) {
       for (int c = 0; c < min(Cfg::RBD, ring_chunks(t)); ++c) ring_issue(t, c);
     };
-    if constexpr (Cfg::RING) {
+    if constexpr (Cfg::RING && !PF_RING_LATE) {
       if (grp < num_tiles) ring_start(grp);
     }
     for (int tile = grp; tile < num_tiles; tile += ngrp) {
@@ -390,6 +398,12 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
           cv[j4] = row_rot ? __ldg(cs4 + j4 * qstride) : make_float4(1.f, 1.f, 1.f, 1.f);
           sv[j4] = row_rot ? __ldg(sn4 + j4 * qstride) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+      }
+      if constexpr (Cfg::RING && PF_RING_LATE) {   // residual loads once the tile's MMAs are done
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        if (lane == 0) tma_store_wait_read<0>();
+        __syncwarp();
+        ring_start(tile);
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -497,7 +511,7 @@ __global__ void __launch_bounds__(GemmCfg<CG, EPI>::THREADS, 1)
         if (rvalid) args.ss_out[(size_t)(tile % args.num_n_blk) * args.ss_ld + grow] = ssq;
         // start the next tile's residual loads now; they land while its MMAs run
         const int nt = tile + ngrp;
-        if (nt < num_tiles) {
+        if (!PF_RING_LATE && nt < num_tiles) {
           if (lane == 0) tma_store_wait_read<0>();
           __syncwarp();
           ring_start(nt);
